@@ -1,0 +1,441 @@
+#!/usr/bin/env python3
+"""Benchmark of the CPI hot path (TPA preprocessing + batched online RWR queries).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One *step* is one pass of the hot path over one job of the chosen BASELINE
+config: PageRank preprocessing (the stranger vector, 116 sweeps at c=0.15,
+eps=1e-9) followed by the config's online queries (1,024 seeds at C2) in SpMM
+batches (32 at C2), S=5, T=10.  Inputs (graph CSR, seeds) are resident on the
+device before the timed region; outputs stay in HBM.  Between timed steps the
+L2 is flushed (a 512 MiB write, outside the events).
+
+Metric (BASELINE.json): CPI edges/s (GTEPS) -- algorithmic edge traversals
+m * (sweeps x active columns) per second -- with queries/s and the HBM
+roofline fraction of the dominant sweep kernel reported beside it.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/librwrank_ref.so, built from /root/reference/proj/src; the C
+oracle port if that is absent) on the host cores, same config and metric.
+
+Multi-GPU (torchrun, one rank per GPU): seed-parallel replicas -- every rank
+holds the graph, preprocesses, and answers its own full query set (weak
+scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C, EPS, S, T = 0.15, 1e-9, 5, 10
+
+CONFIGS = {
+    # name: (kind, params, queries, batch, rng seed)
+    "c1": ("rmat", dict(scale=16, edge_factor=16), 1, 1, 1),
+    "c2": ("rmat", dict(scale=20, edge_factor=16), 1024, 32, 1),
+    "c3": ("er", dict(n=4194304, m=67108864), 4096, 64, 1),
+    "c4": ("rmat", dict(scale=24, edge_factor=32), 1024, 32, 1),
+    "c5": ("rmat", dict(scale=28, edge_factor=16), 256, 16, 1),
+}
+DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1]: the metric's single-GPU workload
+THROTTLE_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def build_graph(cfg_name):
+    import paper_1708_02574_b200 as P
+    kind, p, *_ = CONFIGS[cfg_name]
+    if kind == "rmat":
+        return P.generate_rmat(p["scale"], p["edge_factor"], 0.57, 0.19, 0.19, rng_seed=CONFIGS[cfg_name][4])
+    return P.generate_random_graph(p["n"], p["m"], CONFIGS[cfg_name][4])
+
+
+def workload_desc(cfg_name, g, nq, batch):
+    kind, p, *_ = CONFIGS[cfg_name]
+    gdesc = (f"R-MAT scale {p['scale']} ef {p['edge_factor']} (a,b,c)=(.57,.19,.19), mt19937_64 seed "
+             f"{CONFIGS[cfg_name][4]}, no noise/permutation" if kind == "rmat"
+             else f"ER G(n,m) n={p['n']} m={p['m']} (generate_random_graph seed {CONFIGS[cfg_name][4]})")
+    return {
+        "workload": f"{cfg_name.upper()}: TPA preprocess (PageRank CPI, window [T,inf)) + {nq} online queries "
+                    f"in SpMM batches of {batch}",
+        "graph": gdesc, "n": g.node_count(), "m": g.edge_count(), "dangling": int(len(g.dangling_nodes())),
+        "policy": "selfloop", "c": C, "eps": EPS, "S": S, "T": T, "queries": nq, "batch": batch,
+        "seeds": "sample_seeds(mt19937_64 seed 1): uniform over non-dangling nodes (rwrank_main.cpp:65-83)",
+        "l2": "flushed between timed steps (512 MiB write, untimed)",
+    }
+
+
+def a_step(n, m, B, acc):
+    """SURVEY §8(d) algorithmic bytes of one CPI sweep over B columns."""
+    return 4 * m + 8 * (n + 1) + 8 * n + 8 * B * n * (2 + 2 * acc)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m_, r = float(parts[0]), float(parts[1]), int(parts[2], 16)
+            except ValueError:
+                continue
+            mx = m_
+            if r & ~0x1:  # ignore gpu_idle samples
+                for bit, name in THROTTLE_BITS.items():
+                    if r & bit and bit != 0x1:
+                        reasons.add(name)
+            if not (r == 0x1):
+                sm.append(s)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.lines)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_per_launch(kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU arm (reference library, or the oracle port)
+# ---------------------------------------------------------------------------
+def cpu_measure(g, seeds, cfg_name, budget_s=20.0, workers=None):
+    """Times the reference CPU path on a bounded sample of the job and
+    extrapolates the job time.  Returns a dict (cpu_baseline)."""
+    from oracle import Oracle, Reference
+    n, m = g.node_count(), g.edge_count()
+    nq = len(seeds)
+    workers = workers or os.cpu_count() or 1
+    if Reference.available():
+        ref = Reference()
+        off = g.out_offsets().astype(np.int64)
+        src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(off))
+        rg = ref.graph_from_edges(n, src, g.out_targets(), "selfloop")
+        assert rg.fingerprint == g.fingerprint()
+        kind = "reference"
+        # preprocess: one full reference call (threads=1: the reference default;
+        # its threaded sweep is slower at these sizes); time-box
+        # large graphs to a few dense sweeps and extrapolate x sweeps.
+        t_sweep = rg.time_sweeps(1, C, 1)
+        if t_sweep * 117 <= budget_s * 0.6:
+            stranger, t_pre = rg.time_preprocess(C, EPS, T, 1, keep=True)
+            pre_note = "preprocess timed whole"
+        else:
+            k = max(1, min(3, int(budget_s * 0.3 / max(t_sweep, 1e-9))))
+            t_pre = rg.time_sweeps(k, C, 1) / k * 116
+            stranger = np.zeros(n)
+            pre_note = f"preprocess extrapolated from {k} dense sweeps x 116"
+        # queries: concurrent reference query() calls on all host threads
+        est_q = max(t_sweep * 0.3, 1e-4)
+        nsample = int(max(workers, min(nq, budget_s * 0.4 / est_q * workers)))
+        nsample = min(nq, max(1, nsample))
+        _, t_q = rg.query_many(stranger, C, EPS, T, seeds[:nsample], S, workers)
+        t_job = t_pre + t_q * nq / nsample
+        sample = (f"{pre_note} (threads=1) + {nsample} of {nq} queries on {workers} threads "
+                  f"(reference query(), concurrent), job time extrapolated")
+    else:
+        orc = Oracle()
+        kind = "port"
+        workers = 1
+        t0 = time.perf_counter()
+        stranger = orc.preprocess(g, C, EPS, T)
+        t_pre = time.perf_counter() - t0
+        nsample = min(nq, 8)
+        t0 = time.perf_counter()
+        for s in seeds[:nsample]:
+            orc.query(g, stranger, C, EPS, T, int(s), S)
+        t_q = time.perf_counter() - t0
+        t_job = t_pre + t_q * nq / nsample
+        sample = f"oracle port: preprocess whole + {nsample} of {nq} queries serial, extrapolated"
+    edges = m * (116 + 4 * nq)
+    return {"value": edges / t_job / 1e9, "unit": "GTEPS", "cores": int(workers), "kind": kind,
+            "sample": sample, "job_s": t_job, "preprocess_s": t_pre,
+            "queries_per_s": nq / (t_job - t_pre) if t_job > t_pre else None}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg_name = args.config
+    _, _, nq, batch, seed = CONFIGS[cfg_name]
+    import paper_1708_02574_b200 as P
+    g = build_graph(cfg_name)
+    seeds = P.sample_seeds(g, nq, seed)
+    vals = []
+    cb = None
+    steps = max(1, args.steps)
+    for i in range(max(0, args.warmup) + steps):
+        budget = 20.0 if i >= args.warmup else 5.0
+        r = cpu_measure(g, seeds, cfg_name, budget_s=budget)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            cb = r
+    v = statistics.median(vals)
+    cb = dict(cb, value=v)
+    line = {"impl": "reference", "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",
+            "value": v, "unit": "GTEPS", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": cb["job_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(cfg_name, g, nq, batch), "queries_per_s": cb["queries_per_s"],
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1708_02574_b200 as P
+    from paper_1708_02574_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    cfg_name = args.config
+    _, _, nq, batch, seed = CONFIGS[cfg_name]
+    t0 = time.perf_counter()
+    g = build_graph(cfg_name)
+    t_build = time.perf_counter() - t0
+    n, m = g.node_count(), g.edge_count()
+    all_seeds = P.sample_seeds(g, nq * world, seed)
+    seeds = np.ascontiguousarray(all_seeds[rank * nq:(rank + 1) * nq])
+    log(f"[rank {rank}] graph {cfg_name}: n={n} m={m} built in {t_build:.1f}s")
+
+    t0 = time.perf_counter()
+    dg = g.device(local)
+    torch.cuda.synchronize()
+    t_ingest = time.perf_counter() - t0
+    stream = torch.cuda.current_stream(dev)
+    dg.set_stream(stream.cuda_stream)
+    lib = N.lib
+    h = dg.h
+    import ctypes as C_
+
+    out = torch.empty((batch, n), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    batches = [np.ascontiguousarray(seeds[i:i + batch]) for i in range(0, nq, batch)]
+
+    def device_step():
+        art = C_.c_void_p()
+        N.check(lib.tpa_preprocess(h, C, EPS, T, None, C_.byref(art), N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
+        for b in batches:
+            N.check(lib.tpa_query_batch(h, art, b.ctypes.data, len(b), S, out.data_ptr(),
+                                        N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
+        return art
+
+    # warm-up
+    for _ in range(args.warmup):
+        a = device_step()
+        lib.tpa_artifact_destroy(a)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    launches0 = dg.launches()
+    times = []
+    dg.profile(True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            a = device_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            lib.tpa_artifact_destroy(a)
+    launches = dg.launches() - launches0
+    mv_cnt, mv_ms = dg.profile_read(1)
+    mm_cnt, mm_ms = dg.profile_read(batch if batch > 1 else 1)
+    dg.profile(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(times)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+
+    # sweeps actually run: 116 PageRank sweeps (the convergence break) + (S-1) per query
+    pr = P.pagerank(g, P.CpiParams(C, EPS))
+    pre_sweeps = pr.iterations_run
+    edges_per_step = m * (pre_sweeps + (S - 1) * nq)
+    value = edges_per_step * world * args.steps / (total_ms / 1e3) / 1e9
+    qps = nq * world * args.steps / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (the SpMM sweep at batch width B)
+    peak, peak_src = peak_hbm()
+    Bk = batch if batch > 1 else 1
+    if batch > 1 and mm_cnt:
+        kname = f"k_step_spmm<{Bk}>"
+        # 3 of 4 query sweeps accumulate; the 4th is the fused combine (same A_step class)
+        bytes_launch = a_step(n, m, Bk, 1)
+        avg_ms = mm_ms / mm_cnt
+        share = mm_ms / total_ms if total_ms else None
+    else:
+        kname = "k_step_spmv"
+        bytes_launch = a_step(n, m, 1, 1)
+        avg_ms = mv_ms / max(mv_cnt, 1)
+        share = mv_ms / total_ms if total_ms else None
+    achieved = bytes_launch / (avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": traffic_per_launch(kname), "algorithmic_bytes_per_launch": bytes_launch,
+                "avg_launch_ms": avg_ms, "launches_timed": mm_cnt if batch > 1 else mv_cnt,
+                "share_of_step": share,
+                "spmv": {"launches": mv_cnt, "avg_ms": mv_ms / max(mv_cnt, 1),
+                         "achieved_gbs": a_step(n, m, 1, 1) / (mv_ms / max(mv_cnt, 1) / 1e3) / 1e9
+                         if mv_cnt else None}}
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        host_out = torch.empty((batch, n), dtype=torch.float64, pin_memory=True)
+        host_str = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        h2d = d2h = 0
+        el = []
+        for _ in range(e2e_steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            art = C_.c_void_p()
+            N.check(lib.tpa_preprocess(h, C, EPS, T, host_str.data_ptr(), C_.byref(art), 0))
+            d2h_s = n * 8
+            h2d_s = 0
+            for b in batches:
+                N.check(lib.tpa_query_batch(h, art, b.ctypes.data, len(b), S, host_out.data_ptr(), 0))
+                h2d_s += len(b) * 4
+                d2h_s += len(b) * n * 8
+            torch.cuda.synchronize()
+            el.append(time.perf_counter() - t0)
+            lib.tpa_artifact_destroy(art)
+            h2d, d2h = h2d_s, d2h_s
+        tt = torch.tensor([sum(el)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": edges_per_step * world * e2e_steps / float(tt.item()) / 1e9, "unit": "GTEPS",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "queries_per_s": nq * world * e2e_steps / float(tt.item()),
+               "steps": e2e_steps, "ms_per_step": float(tt.item()) / e2e_steps * 1e3,
+               "note": "C-ABI with host buffers: seeds from host, stranger + every full score vector "
+                       "copied back to pinned host memory (the reference API returns ScoreVectors)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_measure(g, seeds, cfg_name, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",
+            "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg_name, g, nq, batch),
+            "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "ingest_s": t_ingest, "graph_build_s": t_build,
+            "parallelism": f"seed-parallel replicas x{world}" if world > 1 else "single GPU",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,184 @@
+/*
+ * tpa_gpu.h -- C-ABI of the B200-native CPI engine (libtpa_gpu.so).
+ *
+ * Drop-in boundary for the reference's hot path: the C++ entry points of
+ * /root/reference/proj/include/rwrank/{cpi,tpa,graph}.hpp.  Every function
+ * below names the reference interface it replaces.  Plain pointers and sizes
+ * only: no C++ or torch types cross this boundary.
+ *
+ * Status codes mirror the reference's exception types:
+ *   TPA_OK                    0
+ *   TPA_ERR_INVALID_ARGUMENT  1  std::invalid_argument
+ *   TPA_ERR_OUT_OF_RANGE      2  std::out_of_range
+ *   TPA_ERR_RUNTIME           3  std::runtime_error ("stale artifact: ...")
+ *   TPA_ERR_CUDA              4  device/driver failure
+ *   TPA_ERR_ALLOC             5  device allocation failure
+ * The message of the last failure on the calling thread is tpa_last_error();
+ * parameter errors use the reference's own message text.
+ *
+ * Threading: a tpa_graph serialises its own calls (one stream per handle);
+ * results are deterministic, so concurrent callers get bitwise-identical
+ * vectors (tpa_test.cpp:148-161).  The reference's `threads` argument selects
+ * host parallelism; here it has no meaning and is not taken.
+ *
+ * Memory: unless TPA_DEVICE_PTRS is set, vector arguments are host pointers
+ * (pinned or pageable).  With TPA_DEVICE_PTRS they are device pointers on the
+ * handle's device and the call returns without a host synchronisation when
+ * nothing has to come back to the host (TPA_ASYNC).
+ */
+#ifndef TPA_GPU_H
+#define TPA_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPA_ABI_VERSION 1
+
+enum tpa_status {
+    TPA_OK = 0,
+    TPA_ERR_INVALID_ARGUMENT = 1,
+    TPA_ERR_OUT_OF_RANGE = 2,
+    TPA_ERR_RUNTIME = 3,
+    TPA_ERR_CUDA = 4,
+    TPA_ERR_ALLOC = 5
+};
+
+/* rwrank::DanglingPolicy (graph.hpp:19), declaration order. */
+enum tpa_policy { TPA_SELFLOOP = 0, TPA_UNIFORM = 1, TPA_DROP = 2 };
+
+enum tpa_flags {
+    TPA_DEVICE_PTRS = 1,  /* vector in/out arguments are device pointers */
+    TPA_ASYNC = 2,        /* with TPA_DEVICE_PTRS: do not synchronise on return */
+    TPA_NODE_MAJOR = 4,   /* batch output laid out [n][B] instead of [B][n] */
+    TPA_QUERY_NA = 8      /* query_batch: no stranger term (tpa.cpp:78-86) */
+};
+
+typedef struct tpa_graph tpa_graph;       /* device-resident CSR(A^T) + workspaces */
+typedef struct tpa_artifact tpa_artifact; /* device-resident StrangerArtifact */
+
+int tpa_abi_version(void);
+const char *tpa_last_error(void);
+
+/* --- graph ---------------------------------------------------------------
+ * Replaces: the rwrank::Graph a caller hands to every entry point
+ * (graph.hpp:26-66).  Input is the reference Graph's out-edge CSR exactly as
+ * out_offsets()/out_targets() return it (graph.hpp:45-46): sorted, deduped,
+ * SelfLoop repair edges included; policy = dangling_policy(); fingerprint =
+ * fingerprint() (graph.hpp:56).  The GPU ingest builds CSR(A^T) with
+ * ascending sources per row, the out-degree array and the work schedules.
+ * out_offsets/out_targets are host pointers. */
+int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t *out_offsets,
+                     const uint32_t *out_targets, int policy, uint64_t fingerprint, int device,
+                     tpa_graph **out);
+int tpa_graph_destroy(tpa_graph *g);
+/* Make the handle enqueue on an external cudaStream_t (NULL: its own stream). */
+int tpa_graph_set_stream(tpa_graph *g, void *cuda_stream);
+int tpa_graph_info(const tpa_graph *g, uint32_t *n, uint64_t *m, uint64_t *fingerprint,
+                   int *policy, uint64_t *device_bytes);
+/* Number of kernels this handle has launched so far (instrumentation). */
+uint64_t tpa_graph_launches(const tpa_graph *g);
+/* Bench instrumentation: while enabled, every CPI sweep kernel launch is
+ * bracketed by CUDA events on the handle's stream.  enable != 0 starts a new
+ * session.  profile_read sums the recorded launches of the sweep kernel of a
+ * given batch width (1 = SpMV; 8/16/32/64 = SpMM); it synchronises. */
+int tpa_graph_profile(tpa_graph *g, int enable);
+int tpa_graph_profile_read(tpa_graph *g, int width, uint64_t *launches, double *total_ms);
+/* Device copy of CSR(A^T) for inspection: row_ptr[n+1] (int64), col[m]. Host ptrs. */
+int tpa_graph_transpose(const tpa_graph *g, int64_t *row_ptr, uint32_t *col);
+
+/* --- one sweep ------------------------------------------------------------
+ * Replaces: propagation_sweep(g, x, y, c) (graph.hpp:96-103, graph.cpp:230-270).
+ * x, y: n doubles.  0 <= c < 1 else TPA_ERR_INVALID_ARGUMENT. */
+int tpa_propagation_sweep(tpa_graph *g, const double *x, double *y, double c, int flags);
+
+/* --- CPI -------------------------------------------------------------------
+ * Replaces: cpi_run(g, SeedSet(seeds), CpiParams{c, eps, start, terminal})
+ * (cpi.hpp:49, cpi.cpp:87-101); with seeds == NULL: pagerank(g, params)
+ * (cpi.hpp:57, cpi.cpp:111-113).  terminal_iter < 0 means nullopt.
+ * seeds need not be sorted; empty or duplicate -> INVALID_ARGUMENT
+ * (cpi.cpp:19-24); any seed >= n -> OUT_OF_RANGE (cpi.cpp:34-39).
+ * out_scores: n doubles; the other outputs may be NULL. */
+int tpa_cpi_run(tpa_graph *g, const uint32_t *seeds, uint64_t n_seeds, double c, double eps,
+                uint32_t start_iter, int64_t terminal_iter, double *out_scores,
+                uint32_t *iterations_run, int *converged, double *residual_l1, int flags);
+
+/* Replaces: cpi_partition(g, seeds, c, eps, boundaries) (cpi.hpp:60-62,
+ * cpi.cpp:115-136).  out: (n_boundaries + 1) x n doubles, segment-major. */
+int tpa_cpi_partition(tpa_graph *g, const uint32_t *seeds, uint64_t n_seeds, double c, double eps,
+                      const uint32_t *boundaries, uint64_t n_boundaries, double *out, int flags);
+
+/* Batched extension of exact_rwr (cpi.hpp:53-54, cpi.cpp:103-109): B
+ * independent full-window single-seed runs.  out: [B][n] (or [n][B]). */
+int tpa_exact_rwr_batch(tpa_graph *g, const uint32_t *seeds, uint32_t B, double c, double eps,
+                        double *out, int flags);
+
+/* --- TPA -------------------------------------------------------------------
+ * Replaces: neighbor_scale_factor (tpa.hpp:32, tpa.cpp:39-44). */
+double tpa_neighbor_scale_factor(double c, uint32_t S, uint32_t T);
+
+/* Replaces: preprocess(g, c, eps, T) (tpa.hpp:27-28, tpa.cpp:19-37).
+ * T < 1 -> INVALID_ARGUMENT.  out_stranger (n doubles) and out_artifact may
+ * each be NULL; the artifact stays on the device for tpa_query*. */
+int tpa_preprocess(tpa_graph *g, double c, double eps, uint32_t T, double *out_stranger,
+                   tpa_artifact **out_artifact, int flags);
+
+/* A device artifact from a host (or device) StrangerArtifact (tpa.hpp:17-23). */
+int tpa_artifact_create(tpa_graph *g, const double *stranger, uint64_t graph_fingerprint, double c,
+                        double eps, uint32_t T, int flags, tpa_artifact **out);
+int tpa_artifact_destroy(tpa_artifact *a);
+
+/* Replaces: query(g, artifact, seed, S) (tpa.hpp:37-38, tpa.cpp:61-76).
+ * Fingerprint mismatch -> RUNTIME "stale artifact: graph fingerprint
+ * mismatch"; S < 1 or S >= artifact T -> INVALID_ARGUMENT.  out: n doubles. */
+int tpa_query(tpa_graph *g, const tpa_artifact *a, uint32_t seed, uint32_t S, double *out,
+              int flags);
+
+/* B independent query() calls in one batched CPI (SpMM over B seeds).  Same
+ * validation as tpa_query, in the same order.  out: [B][n] unless
+ * TPA_NODE_MAJOR.  With TPA_QUERY_NA the stranger term is omitted and `a`
+ * only supplies c, eps, T (it may then be NULL: see tpa_query_na_batch). */
+int tpa_query_batch(tpa_graph *g, const tpa_artifact *a, const uint32_t *seeds, uint32_t B,
+                    uint32_t S, double *out, int flags);
+
+/* Replaces: query_na(g, seed, TpaParams{S, T, c, eps}) (tpa.hpp:41,
+ * tpa.cpp:78-86), batched over B seeds (B = 1 is query_na itself). */
+int tpa_query_na_batch(tpa_graph *g, const uint32_t *seeds, uint32_t B, uint32_t S, uint32_t T,
+                       double c, double eps, double *out, int flags);
+
+/* --- host-side graph plumbing (not on the hot path) -----------------------
+ * A host graph with the reference Graph's construction semantics
+ * (graph.cpp:53-91: sort, dedupe, pre-policy dangling list, SelfLoop repair,
+ * out-CSR, FNV-1a fingerprint), plus the generators the benchmarks use. */
+typedef struct tpa_host_graph tpa_host_graph;
+
+int tpa_host_graph_from_edges(uint32_t n, const uint32_t *src, const uint32_t *dst, uint64_t m,
+                              int policy, tpa_host_graph **out);
+/* R-MAT 2^scale nodes, edge_factor * 2^scale raw edges, quadrant probs
+ * (a,b,c,1-a-b-c), mt19937_64(seed), no noise, no permutation, self-loops
+ * dropped, duplicates removed by the construction. */
+int tpa_host_graph_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                        uint64_t seed, int policy, int threads, tpa_host_graph **out);
+/* generate_random_graph(n, m, seed, policy) semantics (graph.cpp:166-205). */
+int tpa_host_graph_random(uint32_t n, uint64_t m, uint64_t seed, int policy,
+                          tpa_host_graph **out);
+void tpa_host_graph_destroy(tpa_host_graph *h);
+void tpa_host_graph_info(const tpa_host_graph *h, uint32_t *n, uint64_t *m,
+                         uint64_t *n_dangling, uint64_t *fingerprint, int *policy);
+const uint64_t *tpa_host_graph_offsets(const tpa_host_graph *h);
+const uint32_t *tpa_host_graph_targets(const tpa_host_graph *h);
+const uint32_t *tpa_host_graph_dangling(const tpa_host_graph *h);
+/* Uniform sample without replacement of non-dangling nodes
+ * (rwrank_main.cpp:65-83 sample_seeds, restated). */
+int tpa_sample_seeds(const tpa_host_graph *h, uint64_t count, uint64_t rng_seed, uint32_t *out);
+/* FNV-1a over (n, m, offsets, targets, policy) as graph.cpp:84-90. */
+uint64_t tpa_fingerprint(uint32_t n, uint64_t m, const uint64_t *off, const uint32_t *tgt,
+                         int policy);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPA_GPU_H */

@@ -1,0 +1,572 @@
+// cpi_kernels.cuh -- sm_100a kernels for the Cumulative Power Iteration step.
+//
+// Replaces the reference's CPU hot loop:
+//   propagation_sweep / sweep_range   proj/src/graph.cpp:211-270
+//   l1_sum / add_into / run_series    proj/src/cpi.cpp:43-83
+//   query combine                     proj/src/tpa.cpp:70-74, :84
+//
+// Representation.  The reference pushes x[u]·keep/deg(u) along
+// out-edges.  Here every sweep is a PULL over CSR(Ãᵀ): row v lists its
+// in-neighbours u in ascending order.  The iterate is stored as its *share*
+//   share[u] = (keep · x[u]) / deg(u)            (graph.cpp:222, same rounding)
+// so a sweep is a pure gather-sum  y[v] = Σ_u share[u]  and the n divisions
+// per column happen once per row in the epilogue (not once per edge).  The
+// epilogue of sweep i fuses, per row and column:
+//   + Uniform spread   (graph.cpp:265-268, from the dangling mass of x⁽ⁱ⁻¹⁾)
+//   acc += y           (cpi.cpp:49-51, predicated on the window cpi.cpp:95-96)
+//   out = scale·acc + stranger          (tpa.cpp:73-74, last family sweep)
+//   share_next = keep·y / deg           (input of sweep i+1)
+//   L1 residual and dangling-mass partials (cpi.cpp:74, graph.cpp:218-221)
+// and the last CTA to finish reduces the partials in a FIXED order and
+// advances the per-column convergence state (cpi.cpp:75-80), so no host
+// synchronisation is needed between sweeps and results are deterministic.
+//
+// All fp64 arithmetic goes through __dadd_rn/__dmul_rn/__ddiv_rn so nothing is
+// contracted into an FMA (the reference is compiled without FMA).  Row sums:
+//   SpMM (B >= 8 seeds, lane = column): strictly sequential ascending-source
+//     order for rows <= kMmLongRow, i.e. bitwise the reference's scatter order;
+//     longer rows: 8 fixed chunks, each sequential, combined in chunk order.
+//   SpMV (B = 1): rows <= 32 sequential; longer rows a fixed lane/warp tree.
+// Both orders depend on the row alone, never on timing.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tpa {
+
+constexpr int kSelfLoop = 0, kUniform = 1, kDrop = 2;
+constexpr uint32_t kLongFlag = 0x80000000u;
+constexpr int kThreads = 256;         // CTA size of every step kernel
+constexpr int kGroupItems = 128;      // items per first-level ticket group
+
+// SpMV (B = 1) tiling.
+constexpr int kMvTileNnz = 2048;      // gathered values staged in smem per CTA
+constexpr int kMvTileRows = 512;
+constexpr int kMvShortRow = 32;       // rows <= this: one thread, sequential
+// SpMM (B >= 8) tiling.
+constexpr int kMmTileNnz = 2048;
+constexpr int kMmTileRows = 256;
+constexpr int kMmLongRow = 4096;      // rows above: CTA item, 8 ordered chunks
+constexpr int kMmChunks = 8;
+
+// Per-column CPI state, double-buffered by sweep parity.
+struct ColState {
+    double residual;    // ||x^(iters)||_1
+    double spread;      // Uniform: (keep*dm)/n added by the next sweep
+    uint32_t iters;     // index of the last interim vector computed
+    int32_t active;     // next sweep computes this column
+    int32_t converged;  // tolerance break fired
+    int32_t has_spread; // dm != 0 under Uniform
+};
+
+struct StepArgs {
+    const int64_t* __restrict__ row_ptr;  // CSR(Ãᵀ) n+1
+    const uint32_t* __restrict__ col;     // m, ascending per row
+    const uint32_t* __restrict__ deg;     // out-degree per node (n)
+    const uint2* __restrict__ items;      // {row_begin, row_end | kLongFlag}
+    uint32_t n_items;
+    uint32_t n;
+    int policy;
+    double keep;                          // 1 - c
+    double eps;
+    int64_t terminal;                     // -1: run to convergence
+    uint32_t step;                        // i of x^(i) produced by this sweep
+
+    const double* __restrict__ share_in;  // n x B
+    double* __restrict__ share_out;       // n x B, null on the last sweep
+    double* __restrict__ y_out;           // n x B raw x^(i) (sweep API), or null
+    double* __restrict__ acc;             // n x B, null outside the window
+    double* __restrict__ out;             // combine target, or null
+    const double* __restrict__ stranger;  // n, null for query_na
+    double scale;                         // 1 + nsf
+    int out_node_major;                   // out layout: 1 -> [n][B], 0 -> [B][n]
+    uint32_t b_valid;                     // columns < b_valid are real seeds
+
+    const ColState* state_in;
+    ColState* state_out;
+    double* part;                         // n_items x 2B   (l1 | dm)
+    double* gpart;                        // n_groups x 2B
+    uint32_t* group_cnt;                  // n_groups, zero between launches
+    uint32_t* done_cnt;                   // 1, zero between launches
+};
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) { return __ldg(p); }
+
+// Streaming read of the CSR index array: read once per sweep, keep it out of L1.
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// Deterministic warp sum: xor butterfly, every lane ends with the same value.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic CTA sum (fixed tree); result valid in every thread.
+__device__ __forceinline__ double block_sum(double v, double* s_red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    double r = s_red[0];
+#pragma unroll
+    for (int k = 1; k < kThreads / 32; ++k) r = dadd(r, s_red[k]);
+    __syncthreads();
+    return r;
+}
+
+// Column sums of src[count][2B] (l1 | dm halves) in a fixed order into
+// dst[2B] (shared).  B2 = 2B <= kThreads, power of two.
+__device__ __forceinline__ void ordered_column_sums(const double* src, uint32_t count, int B2,
+                                                    double* s_scr, double* dst) {
+    const int tid = threadIdx.x;
+    const int nsl = kThreads / B2;
+    const int b = tid % B2, sl = tid / B2;
+    const uint32_t per = (count + nsl - 1) / nsl;
+    const uint32_t k0 = sl * per;
+    const uint32_t k1 = min(count, k0 + per);
+    double s = 0.0;
+    for (uint32_t k = k0; k < k1; ++k) s = dadd(s, __ldcg(src + (size_t)k * B2 + b));
+    s_scr[tid] = s;
+    __syncthreads();
+    for (int w = nsl / 2; w > 0; w >>= 1) {
+        if (sl < w) s_scr[tid] = dadd(s_scr[tid], s_scr[tid + w * B2]);
+        __syncthreads();
+    }
+    if (sl == 0) dst[b] = s_scr[b];
+    __syncthreads();
+}
+
+// Publishes this item's (l1 | dm) partials (smem s_part[2B]) and, if it is the
+// last item of its group and then the last group, reduces everything in fixed
+// order and writes the next column state.  Must be reached by all threads.
+__device__ __forceinline__ void finish_item(const StepArgs& a, uint32_t item, int B,
+                                            const double* s_part, double* s_scr,
+                                            double* s_fin) {
+    const int tid = threadIdx.x;
+    const int B2 = 2 * B;
+    __shared__ uint32_t s_ticket;
+    for (int b = tid; b < B2; b += kThreads) a.part[(size_t)item * B2 + b] = s_part[b];
+    __threadfence();
+    __syncthreads();
+    const uint32_t g = item / kGroupItems;
+    const uint32_t g0 = g * kGroupItems;
+    const uint32_t gsize = min((uint32_t)kGroupItems, a.n_items - g0);
+    if (tid == 0) s_ticket = atomicAdd(&a.group_cnt[g], 1u);
+    __syncthreads();
+    if (s_ticket != gsize - 1) return;
+    __threadfence();
+    ordered_column_sums(a.part + (size_t)g0 * B2, gsize, B2, s_scr, s_fin);
+    for (int b = tid; b < B2; b += kThreads) a.gpart[(size_t)g * B2 + b] = s_fin[b];
+    if (tid == 0) a.group_cnt[g] = 0;
+    __threadfence();
+    __syncthreads();
+    const uint32_t n_groups = (a.n_items + kGroupItems - 1) / kGroupItems;
+    if (tid == 0) s_ticket = atomicAdd(a.done_cnt, 1u);
+    __syncthreads();
+    if (s_ticket != n_groups - 1) return;
+    __threadfence();
+    ordered_column_sums(a.gpart, n_groups, B2, s_scr, s_fin);
+    // cpi.cpp:73-80 -- iterations_run, residual, convergence break, terminal.
+    for (int b = tid; b < B; b += kThreads) {
+        ColState s = a.state_in[b];
+        if (s.active) {
+            const double res = s_fin[b];
+            const double dm = s_fin[B + b];
+            s.residual = res;
+            s.iters = a.step;
+            s.converged = res < a.eps;
+            s.active = !s.converged && (a.terminal < 0 || (int64_t)a.step < a.terminal);
+            s.has_spread = (a.policy == kUniform && dm != 0.0);
+            s.spread = s.has_spread ? ddiv(dmul(a.keep, dm), (double)a.n) : 0.0;
+        }
+        a.state_out[b] = s;
+    }
+    if (tid == 0) *a.done_cnt = 0;
+}
+
+// Row/column epilogue shared by both kernels.  idx = storage index of (v, b)
+// in the n x B node-major iterate.  Returns y (= x^(i)[v][b]).
+__device__ __forceinline__ double epilogue(const StepArgs& a, const ColState& st, uint32_t v,
+                                           uint32_t b, int B, size_t idx, double y,
+                                           uint32_t d) {
+    if (st.has_spread) y = dadd(y, st.spread);  // graph.cpp:265-268
+    if (a.y_out) a.y_out[idx] = y;
+    if (a.acc) {
+        const double f = dadd(a.acc[idx], y);   // cpi.cpp:50
+        if (a.out) {
+            if (b < a.b_valid) {
+                const size_t o = a.out_node_major ? idx : (size_t)b * a.n + v;
+                a.out[o] = a.stranger ? dadd(dmul(a.scale, f), a.stranger[v])  // tpa.cpp:73-74
+                                      : dmul(f, a.scale);                     // tpa.cpp:84
+            }
+        } else {
+            a.acc[idx] = f;
+        }
+    }
+    if (a.share_out) a.share_out[idx] = d ? ddiv(dmul(a.keep, y), (double)d) : 0.0;  // graph.cpp:222
+    return y;
+}
+
+// Combine for a column that already stopped before the last family sweep.
+__device__ __forceinline__ void combine_only(const StepArgs& a, uint32_t v, uint32_t b, int B,
+                                             size_t idx) {
+    if (a.out && a.acc && b < a.b_valid) {
+        const double f = a.acc[idx];
+        const size_t o = a.out_node_major ? idx : (size_t)b * a.n + v;
+        a.out[o] = a.stranger ? dadd(dmul(a.scale, f), a.stranger[v]) : dmul(f, a.scale);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: fused CPI sweep, B = 1 (PageRank / single-vector cpi_run / query()).
+// One CTA per work item: a tile of consecutive short rows (<= kMvTileNnz nnz)
+// staged through shared memory, or one long row reduced by the whole CTA.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_step_spmv(StepArgs a) {
+    __shared__ double s_vals[kMvTileNnz];
+    __shared__ int64_t s_rp[kMvTileRows + 1];
+    __shared__ double s_y[kMvTileRows];
+    __shared__ double s_red[kThreads];
+    __shared__ double s_fin[kThreads];
+    __shared__ double s_part[2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t item = blockIdx.x;
+    const ColState st = a.state_in[0];
+    const uint2 it = a.items[item];
+    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
+    const bool is_long = (it.y & kLongFlag) != 0;
+
+    if (!st.active) {
+        // Column stopped earlier: only a pending combine remains (tpa.cpp:73).
+        if (a.out)
+            for (uint32_t v = rb + tid; v < re; v += kThreads) combine_only(a, v, 0, 1, v);
+        if (item == 0 && tid == 0) a.state_out[0] = st;
+        return;
+    }
+
+    double my_l1 = 0.0, my_dm = 0.0;
+    const bool want_dm = a.policy == kUniform;
+
+    if (!is_long) {
+        const uint32_t nrows = re - rb;
+        for (uint32_t r = tid; r <= nrows; r += kThreads) s_rp[r] = a.row_ptr[rb + r];
+        __syncthreads();
+        const int64_t nb = s_rp[0];
+        const int nnz = (int)(s_rp[nrows] - nb);
+        // Gather: coalesced index loads, 8 independent gathers in flight per thread.
+        {
+            constexpr int U = kMvTileNnz / kThreads;
+            uint32_t u[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int k = tid + j * kThreads;
+                u[j] = k < nnz ? ld_stream_u32(a.col + nb + k) : 0u;
+            }
+            double v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int k = tid + j * kThreads;
+                v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int k = tid + j * kThreads;
+                if (k < nnz) s_vals[k] = v[j];
+            }
+        }
+        __syncthreads();
+        // Short rows: one thread, ascending-source sequential sum (reference order).
+        for (uint32_t r = tid; r < nrows; r += kThreads) {
+            const int lo = (int)(s_rp[r] - nb), hi = (int)(s_rp[r + 1] - nb);
+            if (hi - lo <= kMvShortRow) {
+                double s = 0.0;
+                for (int k = lo; k < hi; ++k) s = dadd(s, s_vals[k]);
+                s_y[r] = s;
+            }
+        }
+        // Longer rows of the tile: one warp each, lane-strided + butterfly.
+        for (uint32_t base = warp * 32; base < nrows; base += kThreads) {
+            const uint32_t r = base + lane;
+            const int len = r < nrows ? (int)(s_rp[r + 1] - s_rp[r]) : 0;
+            unsigned mask = __ballot_sync(0xffffffffu, len > kMvShortRow);
+            while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const uint32_t rr = base + j;
+                const int lo = (int)(s_rp[rr] - nb), hi = (int)(s_rp[rr + 1] - nb);
+                double s = 0.0;
+                for (int k = lo + lane; k < hi; k += 32) s = dadd(s, s_vals[k]);
+                s = warp_sum(s);
+                if (lane == 0) s_y[rr] = s;
+            }
+        }
+        __syncthreads();
+        for (uint32_t r = tid; r < nrows; r += kThreads) {
+            const uint32_t v = rb + r;
+            const uint32_t d = __ldg(a.deg + v);
+            const double y = epilogue(a, st, v, 0, 1, v, s_y[r], d);
+            my_l1 = dadd(my_l1, y);
+            if (want_dm && d == 0) my_dm = dadd(my_dm, y);
+        }
+    } else {
+        // One long row: every thread sums a fixed strided subset, then a fixed tree.
+        const int64_t lo = a.row_ptr[rb], hi = a.row_ptr[rb + 1];
+        double s = 0.0;
+        constexpr int U = 8;
+        int64_t e = lo + tid;
+        for (; e + (U - 1) * kThreads < hi; e += U * kThreads) {
+            uint32_t u[U];
+            double v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) u[j] = ld_stream_u32(a.col + e + j * kThreads);
+#pragma unroll
+            for (int j = 0; j < U; ++j) v[j] = __ldg(a.share_in + u[j]);
+#pragma unroll
+            for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
+        }
+        for (; e < hi; e += kThreads) s = dadd(s, __ldg(a.share_in + ld_stream_u32(a.col + e)));
+        s = block_sum(s, s_red);
+        if (tid == 0) {
+            const uint32_t d = __ldg(a.deg + rb);
+            const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
+            my_l1 = y;
+            if (want_dm && d == 0) my_dm = y;
+        }
+    }
+    const double l1 = block_sum(my_l1, s_red);
+    const double dm = want_dm ? block_sum(my_dm, s_red) : 0.0;
+    if (tid == 0) {
+        s_part[0] = l1;
+        s_part[1] = dm;
+    }
+    __syncthreads();
+    finish_item(a, item, 1, s_part, s_red, s_fin);
+}
+
+// ---------------------------------------------------------------------------
+// K3: fused CPI sweep, B seeds at once (B in {8,16,32,64}); iterate row-major
+// n x B so a gather of source u reads B*8 contiguous bytes.  G = min(B,32)
+// lanes per row, CPL = B/G columns per lane.  Lane = column, so each column's
+// row sum is a plain sequential ascending-source chain.
+// ---------------------------------------------------------------------------
+template <int B>
+struct MmVec;
+template <> struct MmVec<8> { static constexpr int G = 8, CPL = 1; };
+template <> struct MmVec<16> { static constexpr int G = 16, CPL = 1; };
+template <> struct MmVec<32> { static constexpr int G = 32, CPL = 1; };
+template <> struct MmVec<64> { static constexpr int G = 32, CPL = 2; };
+
+template <int CPL>
+__device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
+    if constexpr (CPL == 1) {
+        v[0] = __ldg(p);
+    } else {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kThreads) k_step_spmm(StepArgs a) {
+    constexpr int G = MmVec<B>::G, CPL = MmVec<B>::CPL;
+    constexpr int NGRP = kThreads / G;
+    constexpr int U = 8;  // gathers in flight per lane
+    __shared__ double s_red[kThreads * 2 * CPL];  // (l1 | dm) x NGRP x B
+    __shared__ double s_fin[kThreads];
+    __shared__ double s_part[2 * B];
+    __shared__ double s_chunk[kMmChunks][B];
+    __shared__ ColState s_st[B];
+    __shared__ int s_any;
+
+    const int tid = threadIdx.x;
+    const int grp = tid / G, gl = tid % G;
+    const uint32_t item = blockIdx.x;
+    const uint2 it = a.items[item];
+    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
+    const bool is_long = (it.y & kLongFlag) != 0;
+
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int b = tid; b < B; b += kThreads) {
+        s_st[b] = a.state_in[b];
+        if (s_st[b].active) s_any = 1;
+    }
+    __syncthreads();
+    if (!s_any) {
+        if (a.out)
+            for (uint32_t v = rb + tid / B; v < re; v += kThreads / B) {
+                const uint32_t b = tid % B;
+                combine_only(a, v, b, B, (size_t)v * B + b);
+            }
+        if (item == 0)
+            for (int b = tid; b < B; b += kThreads) a.state_out[b] = s_st[b];
+        return;
+    }
+
+    const int c0 = gl * CPL;  // first column of this lane
+    ColState my_st[CPL];
+    bool act[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        my_st[c] = s_st[c0 + c];
+        act[c] = my_st[c].active != 0;
+    }
+    const bool want_dm = a.policy == kUniform;
+    double my_l1[CPL], my_dm[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) my_l1[c] = my_dm[c] = 0.0;
+
+    if (!is_long) {
+        // Groups of one warp stay in lock-step: the trip count is the warp max.
+        constexpr int GPW = 32 / G;  // groups (rows) per warp
+        const int warp = tid >> 5;
+        for (uint32_t base = rb + warp * GPW; base < re; base += NGRP) {
+            const uint32_t r = base + (grp % GPW);
+            const bool has_row = r < re;
+            int64_t lo = 0, hi = 0;
+            if (has_row) {
+                lo = __ldg(a.row_ptr + r);
+                hi = __ldg(a.row_ptr + r + 1);
+            }
+            const int len = (int)(hi - lo);
+            int maxlen = len;
+            if constexpr (GPW > 1) maxlen = __reduce_max_sync(0xffffffffu, len);
+            double s[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) s[c] = 0.0;
+            for (int off = 0; off < maxlen; off += G) {
+                const int cnt = min(G, len - off);  // may be <= 0 for this group
+                const uint32_t myidx = gl < cnt ? ld_stream_u32(a.col + lo + off + gl) : 0u;
+                for (int j0 = 0; j0 < G; j0 += U) {
+                    if (j0 >= (maxlen - off)) break;  // warp-uniform
+                    double v[U][CPL];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t u = __shfl_sync(0xffffffffu, myidx, j0 + j, G);
+                        if (j0 + j < cnt) {
+                            ld_cols<CPL>(a.share_in + (size_t)u * B + c0, v[j]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j)
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                }
+            }
+            if (has_row) {
+                const uint32_t d = __ldg(a.deg + r);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const size_t idx = (size_t)r * B + c0 + c;
+                    if (act[c]) {
+                        const double y = epilogue(a, my_st[c], r, c0 + c, B, idx, s[c], d);
+                        my_l1[c] = dadd(my_l1[c], y);
+                        if (want_dm && d == 0) my_dm[c] = dadd(my_dm[c], y);
+                    } else {
+                        combine_only(a, r, c0 + c, B, idx);
+                    }
+                }
+            }
+        }
+    } else {
+        // Long row: kMmChunks fixed chunks (function of the row length only),
+        // each summed sequentially by one group, then combined in chunk order.
+        const int64_t lo = __ldg(a.row_ptr + rb), hi = __ldg(a.row_ptr + rb + 1);
+        const int64_t len = hi - lo;
+        if (grp < kMmChunks) {
+            const int64_t c_lo = lo + len * grp / kMmChunks;
+            const int64_t c_hi = lo + len * (grp + 1) / kMmChunks;
+            double s[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) s[c] = 0.0;
+            for (int64_t off = c_lo; off < c_hi; off += G) {
+                const int cnt = (int)min((int64_t)G, c_hi - off);
+                const uint32_t myidx = gl < cnt ? ld_stream_u32(a.col + off + gl) : 0u;
+                for (int j0 = 0; j0 < cnt; j0 += U) {
+                    double v[U][CPL];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t u = __shfl_sync(0xffffffffu >> (32 - G) << ((tid & 31) / G * G),
+                                                       myidx, j0 + j, G);
+                        if (j0 + j < cnt) {
+                            ld_cols<CPL>(a.share_in + (size_t)u * B + c0, v[j]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j)
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) s_chunk[grp][c0 + c] = s[c];
+        }
+        __syncthreads();
+        if (tid < B) {
+            double y = s_chunk[0][tid];
+#pragma unroll
+            for (int k = 1; k < kMmChunks; ++k) y = dadd(y, s_chunk[k][tid]);
+            s_chunk[0][tid] = y;
+        }
+        __syncthreads();
+        // Epilogue by the lanes of group 0 so the per-lane partial layout holds.
+        if (grp == 0) {
+            const uint32_t d = __ldg(a.deg + rb);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const size_t idx = (size_t)rb * B + c0 + c;
+                if (act[c]) {
+                    const double y = epilogue(a, my_st[c], rb, c0 + c, B, idx, s_chunk[0][c0 + c], d);
+                    my_l1[c] = y;
+                    if (want_dm && d == 0) my_dm[c] = y;
+                } else {
+                    combine_only(a, rb, c0 + c, B, idx);
+                }
+            }
+        }
+    }
+    // Per-column partials: groups in fixed order (tree over groups).
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        s_red[grp * B + c0 + c] = my_l1[c];
+        s_red[NGRP * B + grp * B + c0 + c] = my_dm[c];
+    }
+    __syncthreads();
+    for (int w = NGRP / 2; w > 0; w >>= 1) {
+        for (int t = tid; t < w * B; t += kThreads) {
+            s_red[t] = dadd(s_red[t], s_red[t + w * B]);
+            s_red[NGRP * B + t] = dadd(s_red[NGRP * B + t], s_red[NGRP * B + t + w * B]);
+        }
+        __syncthreads();
+    }
+    for (int b = tid; b < B; b += kThreads) {
+        s_part[b] = s_red[b];
+        s_part[B + b] = s_red[NGRP * B + b];
+    }
+    __syncthreads();
+    finish_item(a, item, B, s_part, s_red, s_fin);
+}
+
+}  // namespace tpa

@@ -1,0 +1,1157 @@
+// tpa_gpu.cu -- libtpa_gpu.so: GPU ingest, CPI driver and the C-ABI of
+// include/tpa_gpu.h.  The hot kernels live in cpi_kernels.cuh.
+//
+// Device layout of a graph handle:
+//   row_ptr  int64[n+1]  CSR(Ãᵀ) row offsets (row v = in-neighbours of v)
+//   col      uint32[m]   sources, ascending within each row
+//   deg      uint32[n]   out-degree (after SelfLoop repair)
+//   items    uint2[]     work schedule per kernel family (SpMV, SpMM)
+// Per-width workspace (B = 1, 8, 16, 32, 64): share ping-pong [n][B] fp64,
+// acc [n][B] fp64, reduction partials, ticket counters, ColState x2.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "cpi_kernels.cuh"
+#include "tpa_gpu.h"
+#include "tpa_internal.hpp"
+
+namespace tpa {
+
+std::string& last_error() {
+    thread_local std::string s;
+    return s;
+}
+
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess) {                                                         \
+            cudaGetLastError(); /* consume it: never leak into a later launch check */   \
+            throw ::tpa::cuda_error(std::string(#x) + ": " + cudaGetErrorString(e_));    \
+        }                                                                                \
+    } while (0)
+
+// After a kernel launch: name the kernel in the error.
+#define CKL(name)                                                                        \
+    do {                                                                                 \
+        cudaError_t e_ = cudaGetLastError();                                             \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::tpa::cuda_error(std::string("launch of ") + name + ": " +            \
+                                    cudaGetErrorString(e_));                             \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Device memory
+// ---------------------------------------------------------------------------
+// Stream-ordered allocation (cudaMallocAsync pool): allocating and freeing
+// never synchronises the device, so per-call temporaries and artifacts are
+// cheap and the query pipeline stays asynchronous.
+// The buffer remembers the owning handle's stream *variable*, so frees follow
+// the handle if tpa_graph_set_stream switches streams.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    const cudaStream_t* sp = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, *sp);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t nbytes, const cudaStream_t& stream) {
+        if (bytes >= nbytes && p) return;
+        release();
+        const size_t want = nbytes ? nbytes : 16;
+        if (cudaMallocAsync(&p, want, stream) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            throw alloc_error("cudaMallocAsync of " + std::to_string(want) + " bytes failed");
+        }
+        sp = &stream;
+        bytes = want;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// K1: ingest -- out-edge CSR -> CSR(Ãᵀ) (stable radix sort by target keeps
+// sources ascending inside every row: the reference's scatter order).
+// ---------------------------------------------------------------------------
+__global__ void k_degrees(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ deg) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+         u += (uint64_t)gridDim.x * blockDim.x)
+        deg[u] = (uint32_t)(off[u + 1] - off[u]);
+}
+
+// One warp per source u writes u into its out-edge slots.
+__global__ void k_expand_src(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ src) {
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t u = warp; u < n; u += nwarps)
+        for (uint64_t e = off[u] + lane; e < off[u + 1]; e += 32) src[e] = (uint32_t)u;
+}
+
+// row_ptr[v] = first position of key v in the sorted targets (lower bound).
+__global__ void k_row_ptr(const uint32_t* __restrict__ keys, uint64_t m, uint32_t n,
+                          int64_t* __restrict__ row_ptr) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        row_ptr[v] = (int64_t)lo;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: initial iterate x⁽⁰⁾ (cpi.cpp:59-67).
+// ---------------------------------------------------------------------------
+// Dense B = 1 start: PageRank (x == null: every node gets `weight`,
+// SeedSet::all_nodes) or an explicit x (propagation_sweep / multi-seed sets).
+__global__ void __launch_bounds__(kThreads)
+k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
+             const uint32_t* __restrict__ deg, double keep, double* __restrict__ share0,
+             double* __restrict__ acc0, double* __restrict__ part) {
+    __shared__ double s_red[kThreads];
+    double l1 = 0.0, dm = 0.0;
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = blockIdx.x * per, hi = min((uint64_t)n, lo + per);
+    for (uint64_t u = lo + threadIdx.x; u < hi; u += kThreads) {
+        const double xv = x ? x[u] : weight;
+        const uint32_t d = deg[u];
+        share0[u] = d ? ddiv(dmul(keep, xv), (double)d) : 0.0;
+        if (acc0) acc0[u] = xv;
+        l1 = dadd(l1, fabs(xv));
+        if (d == 0) dm = dadd(dm, xv);
+    }
+    l1 = block_sum(l1, s_red);
+    dm = block_sum(dm, s_red);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = l1;
+        part[2 * blockIdx.x + 1] = dm;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_init_finish(const double* __restrict__ part, uint32_t nblocks, int policy, double keep,
+              uint32_t n, int active0, ColState* state0) {
+    __shared__ double s_scr[kThreads];
+    __shared__ double s_fin[2];
+    ordered_column_sums(part, nblocks, 2, s_scr, s_fin);
+    if (threadIdx.x == 0) {
+        ColState s;
+        s.residual = s_fin[0];
+        s.iters = 0;
+        s.active = active0;
+        s.converged = 0;
+        s.has_spread = policy == kUniform && s_fin[1] != 0.0;
+        s.spread = s.has_spread ? ddiv(dmul(keep, s_fin[1]), (double)n) : 0.0;
+        state0[0] = s;
+    }
+}
+
+// Up to 64 seeds travel as a kernel parameter: no host->device copy, so
+// back-to-back query batches never wait on a staging buffer.
+struct SeedList {
+    uint32_t s[64];
+};
+
+// Batch of single-seed starts x⁽⁰⁾_b = c·e_{seed_b}; share0/acc0 pre-zeroed.
+__global__ void k_init_seeds(const SeedList seeds, uint32_t b_valid, int B, double c,
+                             double keep, uint32_t n, int policy, const uint32_t* __restrict__ deg,
+                             double* __restrict__ share0, double* __restrict__ acc0, int active0,
+                             ColState* state0) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    ColState s;
+    s.iters = 0;
+    s.converged = 0;
+    if (b < (int)b_valid) {
+        const uint32_t seed = seeds.s[b];
+        const uint32_t d = deg[seed];
+        const double w = c;  // c / |S| with |S| = 1
+        share0[(size_t)seed * B + b] = d ? ddiv(dmul(keep, w), (double)d) : 0.0;
+        if (acc0) acc0[(size_t)seed * B + b] = w;
+        s.residual = w;
+        s.active = active0;
+        s.has_spread = policy == kUniform && d == 0;
+        s.spread = s.has_spread ? ddiv(dmul(keep, w), (double)n) : 0.0;
+    } else {
+        s.residual = 0.0;
+        s.active = 0;
+        s.has_spread = 0;
+        s.spread = 0.0;
+    }
+    state0[b] = s;
+}
+
+// K5 standalone combine (S = 1, or every column stopped before sweep S-1).
+__global__ void k_combine(const double* __restrict__ acc, uint32_t n, int B, uint32_t b_valid,
+                          const double* __restrict__ stranger, double scale, int node_major,
+                          double* __restrict__ out) {
+    const uint64_t total = (uint64_t)n * B;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)(i / B), b = (uint32_t)(i % B);
+        if (b >= b_valid) continue;
+        const double f = acc[i];
+        const size_t o = node_major ? i : (size_t)b * n + v;
+        out[o] = stranger ? dadd(dmul(scale, f), stranger[v]) : dmul(f, scale);
+    }
+}
+
+// [n][B] -> [B][n] for the first b_valid columns.
+__global__ void k_transpose(const double* __restrict__ src, uint32_t n, int B, uint32_t b_valid,
+                            double* __restrict__ dst) {
+    const uint64_t total = (uint64_t)n * B;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)(i / B), b = (uint32_t)(i % B);
+        if (b < b_valid) dst[(size_t)b * n + v] = src[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Work schedules (host, once per graph): long rows first (largest first) so
+// they start early, then tiles of consecutive short rows in row order.
+// ---------------------------------------------------------------------------
+struct Schedule {
+    DevBuf items;
+    uint32_t n_items = 0;
+    uint32_t n_groups = 0;
+};
+
+std::vector<uint2> build_items(const std::vector<int64_t>& rp, uint32_t n, int64_t tile_nnz,
+                               uint32_t tile_rows, int64_t long_row) {
+    std::vector<std::pair<int64_t, uint32_t>> longs;
+    std::vector<uint2> tiles;
+    uint32_t r = 0;
+    while (r < n) {
+        const int64_t L = rp[r + 1] - rp[r];
+        if (L > long_row) {
+            longs.push_back({L, r});
+            ++r;
+            continue;
+        }
+        const uint32_t start = r;
+        int64_t nnz = 0;
+        while (r < n && r - start < tile_rows) {
+            const int64_t L2 = rp[r + 1] - rp[r];
+            if (L2 > long_row) break;
+            if (r > start && nnz + L2 > tile_nnz) break;
+            nnz += L2;
+            ++r;
+            if (nnz >= tile_nnz) break;
+        }
+        tiles.push_back(make_uint2(start, r));
+    }
+    std::stable_sort(longs.begin(), longs.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<uint2> items;
+    items.reserve(longs.size() + tiles.size());
+    for (auto& l : longs) items.push_back(make_uint2(l.second, (l.second + 1) | kLongFlag));
+    items.insert(items.end(), tiles.begin(), tiles.end());
+    return items;
+}
+
+struct Workspace {
+    int B = 0;
+    DevBuf share[2], acc, part, gpart, group_cnt, done_cnt, state;
+};
+
+}  // namespace tpa
+
+using namespace tpa;
+
+struct tpa_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint32_t n = 0;
+    uint64_t m = 0;
+    int policy = 0;
+    uint64_t fingerprint = 0;
+    DevBuf row_ptr, col, deg;
+    Schedule mv, mm;
+    std::map<int, std::unique_ptr<Workspace>> ws;
+    DevBuf init_part;
+    DevBuf out_stage;  // host-output staging for batch calls
+    std::set<tpa_artifact*> artifacts;  // detached (buffers freed) on destroy
+    uint64_t launches = 0;
+    int num_sms = 148;
+    std::mutex mu;
+    // optional per-sweep-kernel CUDA-event timing (bench instrumentation)
+    bool profile = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_events;
+    std::vector<cudaEvent_t> event_pool;
+    cudaEvent_t take_event() {
+        cudaEvent_t e;
+        if (!event_pool.empty()) {
+            e = event_pool.back();
+            event_pool.pop_back();
+        } else {
+            CK(cudaEventCreate(&e));
+        }
+        return e;
+    }
+
+    Workspace& workspace(int B) {
+        auto& p = ws[B];
+        if (!p) {
+            p = std::make_unique<Workspace>();
+            p->B = B;
+        }
+        Workspace& w = *p;
+        const Schedule& s = B == 1 ? mv : mm;
+        const size_t nb = (size_t)n * B * sizeof(double);
+        w.share[0].ensure(nb, stream);
+        w.share[1].ensure(nb, stream);
+        w.acc.ensure(nb, stream);
+        w.part.ensure((size_t)s.n_items * 2 * B * sizeof(double), stream);
+        w.gpart.ensure((size_t)s.n_groups * 2 * B * sizeof(double), stream);
+        if (!w.group_cnt.p) {
+            w.group_cnt.ensure((size_t)s.n_groups * sizeof(uint32_t), stream);
+            w.done_cnt.ensure(sizeof(uint32_t), stream);
+            CK(cudaMemsetAsync(w.group_cnt.p, 0, w.group_cnt.bytes, stream));
+            CK(cudaMemsetAsync(w.done_cnt.p, 0, w.done_cnt.bytes, stream));
+        }
+        w.state.ensure(2 * (size_t)B * sizeof(ColState), stream);
+        return w;
+    }
+};
+
+struct tpa_artifact {
+    tpa_graph* g = nullptr;  // null once the graph is gone (buffers freed then)
+    DevBuf stranger;
+    uint64_t fingerprint = 0;
+    double c = 0.15, eps = 1e-9;
+    uint32_t T = 10;
+};
+
+static void detach_artifact(tpa_artifact* a) {
+    a->stranger.release();
+    a->g = nullptr;
+}
+
+namespace tpa {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+static int grid_for(uint64_t work, int per_block, int max_blocks) {
+    uint64_t b = (work + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > (uint64_t)max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+// Steps needed for ||x⁽ⁱ⁾||₁ = c(1-c)^i < eps (exact for SelfLoop/Uniform,
+// an upper bound for Drop); the driver re-checks the device state after.
+static uint32_t sweeps_estimate(double c, double eps) {
+    const double k = std::ceil(std::log(eps / c) / std::log(1.0 - c));
+    if (!(k >= 1.0)) return 1;
+    if (k > 1e6) return 1000000;
+    return (uint32_t)k;
+}
+
+// cpi.cpp:11-17 (CpiParams::validate)
+static void validate_cpi(double c, double eps, uint32_t start, int64_t terminal) {
+    if (!(c > 0.0 && c < 1.0)) throw std::invalid_argument("restart probability must be in (0, 1)");
+    if (!(eps > 0.0)) throw std::invalid_argument("tolerance must be positive");
+    if (terminal >= 0 && (uint64_t)terminal < start)
+        throw std::invalid_argument("terminal iteration precedes start iteration");
+}
+
+// cpi.cpp:34-39 (SeedSet::validate_against), for a sorted seed list.
+static void validate_seed(uint32_t seed, uint32_t n) {
+    if (seed >= n)
+        throw std::out_of_range("seed id " + std::to_string(seed) + " out of range for graph with " +
+                                std::to_string(n) + " nodes");
+}
+
+enum class Init { Dense, Seeds };
+
+struct RunCfg {
+    int B = 1;
+    uint32_t b_valid = 1;
+    double c = 0.15, eps = 1e-9;
+    uint32_t start = 0;
+    int64_t terminal = -1;
+    Init init = Init::Dense;
+    const double* d_x = nullptr;     // Dense: explicit x⁽⁰⁾ (null -> uniform weight)
+    double weight = 0.0;             // Dense with d_x == null
+    SeedList seeds{};                // Seeds (by value)
+    // accumulation: windowed single acc, or partition segment accs
+    double* acc = nullptr;
+    std::vector<double*> seg_acc;
+    std::vector<uint32_t> bounds;
+    // fused combine at the terminal sweep
+    double* out = nullptr;
+    const double* stranger = nullptr;
+    double scale = 1.0;
+    bool node_major = false;
+    // single-sweep API
+    double* y_out = nullptr;
+    bool want_state = true;
+};
+
+struct RunOut {
+    std::vector<ColState> state;
+};
+
+static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
+    return std::upper_bound(bounds.begin(), bounds.end(), i) - bounds.begin();
+}
+
+static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, int B) {
+    const Schedule& s = B == 1 ? g->mv : g->mm;
+    const dim3 grid(s.n_items), block(kThreads);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g->profile) {
+        e0 = g->take_event();
+        e1 = g->take_event();
+        CK(cudaEventRecord(e0, g->stream));
+    }
+    switch (B) {
+        case 1: k_step_spmv<<<grid, block, 0, g->stream>>>(a); break;
+        case 8: k_step_spmm<8><<<grid, block, 0, g->stream>>>(a); break;
+        case 16: k_step_spmm<16><<<grid, block, 0, g->stream>>>(a); break;
+        case 32: k_step_spmm<32><<<grid, block, 0, g->stream>>>(a); break;
+        case 64: k_step_spmm<64><<<grid, block, 0, g->stream>>>(a); break;
+        default: throw std::invalid_argument("unsupported batch width");
+    }
+    CKL("k_step (sweep)");
+    ++g->launches;
+    if (g->profile) {
+        CK(cudaEventRecord(e1, g->stream));
+        g->prof_events.push_back({B, {e0, e1}});
+    }
+}
+
+// The CPI driver: x⁽⁰⁾, then sweeps 1..K enqueued without host syncs; the
+// per-column state (cpi.cpp:70-81) advances on the device.  Only a run to
+// convergence (terminal < 0) checks the state on the host after the
+// estimated horizon, and continues if a column is still active.
+static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
+    const int B = cfg.B;
+    Workspace& w = g->workspace(B);
+    const Schedule& sch = B == 1 ? g->mv : g->mm;
+    const uint32_t n = g->n;
+    const double keep = 1.0 - cfg.c;
+    ColState* st = w.state.as<ColState>();
+    const bool partition = !cfg.bounds.empty() || !cfg.seg_acc.empty();
+
+    // accumulator for x⁽⁰⁾, zero the rest
+    double* acc0 = nullptr;
+    if (partition) {
+        const size_t s0 = seg_of(cfg.bounds, 0);
+        for (size_t k = 0; k < cfg.seg_acc.size(); ++k)
+            if (k != s0 || cfg.init == Init::Seeds)
+                CK(cudaMemsetAsync(cfg.seg_acc[k], 0, (size_t)n * B * 8, g->stream));
+        acc0 = cfg.seg_acc[s0];
+    } else if (cfg.acc) {
+        const bool in0 = cfg.start == 0;
+        if (!in0 || cfg.init == Init::Seeds)
+            CK(cudaMemsetAsync(cfg.acc, 0, (size_t)n * B * 8, g->stream));
+        acc0 = in0 ? cfg.acc : nullptr;
+    }
+    const int active0 = cfg.terminal != 0;
+    if (cfg.init == Init::Dense) {
+        const int nblk = grid_for(n, 4 * kThreads, 4 * g->num_sms);
+        g->init_part.ensure((size_t)nblk * 2 * sizeof(double), g->stream);
+        k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.d_x, cfg.weight, n, g->deg.as<uint32_t>(), keep,
+                                                       w.share[0].as<double>(), acc0,
+                                                       g->init_part.as<double>());
+        CKL("k_init_dense");
+        k_init_finish<<<1, kThreads, 0, g->stream>>>(g->init_part.as<double>(), nblk, g->policy, keep, n,
+                                                     active0, st);
+        CKL("k_init_finish");
+        g->launches += 2;
+    } else {
+        CK(cudaMemsetAsync(w.share[0].p, 0, (size_t)n * B * 8, g->stream));
+        k_init_seeds<<<1, 64, 0, g->stream>>>(cfg.seeds, cfg.b_valid, B, cfg.c, keep, n, g->policy,
+                                              g->deg.as<uint32_t>(), w.share[0].as<double>(), acc0,
+                                              active0, st);
+        CKL("k_init_seeds");
+        g->launches += 1;
+    }
+
+    StepArgs a{};
+    a.row_ptr = g->row_ptr.as<int64_t>();
+    a.col = g->col.as<uint32_t>();
+    a.deg = g->deg.as<uint32_t>();
+    a.items = sch.items.as<uint2>();
+    a.n_items = sch.n_items;
+    a.n = n;
+    a.policy = g->policy;
+    a.keep = keep;
+    a.eps = cfg.eps;
+    a.terminal = cfg.terminal;
+    a.stranger = cfg.stranger;
+    a.scale = cfg.scale;
+    a.out_node_major = cfg.node_major ? 1 : 0;
+    a.b_valid = cfg.b_valid;
+    a.part = w.part.as<double>();
+    a.gpart = w.gpart.as<double>();
+    a.group_cnt = w.group_cnt.as<uint32_t>();
+    a.done_cnt = w.done_cnt.as<uint32_t>();
+
+    const int64_t target = cfg.terminal >= 0 ? cfg.terminal : std::numeric_limits<int64_t>::max();
+    const uint32_t est = sweeps_estimate(cfg.c, cfg.eps);
+    uint64_t done = 0;
+    bool combined = false;
+    int64_t chunk = std::min<int64_t>(target, (int64_t)est + 1);
+    std::vector<ColState> hst(B);
+    while (chunk > 0) {
+        for (int64_t j = 0; j < chunk; ++j) {
+            const uint32_t i = (uint32_t)(done + 1 + j);
+            a.step = i;
+            a.share_in = w.share[(i - 1) & 1].as<double>();
+            const bool last = (int64_t)i == target;
+            a.share_out = (last || cfg.y_out) ? nullptr : w.share[i & 1].as<double>();
+            a.y_out = cfg.y_out;
+            if (partition) {
+                a.acc = cfg.seg_acc[seg_of(cfg.bounds, i)];
+            } else {
+                const bool inw = i >= cfg.start && (cfg.terminal < 0 || (int64_t)i <= cfg.terminal);
+                a.acc = inw ? cfg.acc : nullptr;
+            }
+            a.out = (last && cfg.out) ? cfg.out : nullptr;
+            combined = combined || a.out != nullptr;
+            a.state_in = st + ((i - 1) & 1) * B;
+            a.state_out = st + (i & 1) * B;
+            launch_step(g, w, a, B);
+        }
+        done += chunk;
+        if ((int64_t)done >= target) break;
+        CK(cudaMemcpyAsync(hst.data(), st + (done & 1) * B, B * sizeof(ColState),
+                           cudaMemcpyDeviceToHost, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+        bool any = false;
+        for (int b = 0; b < B; ++b) any = any || hst[b].active;
+        if (!any) break;
+        chunk = std::min<int64_t>(target - (int64_t)done, 16);
+    }
+    if (cfg.out && !combined) {
+        double* acc_final = cfg.acc;
+        k_combine<<<grid_for((uint64_t)n * B, 256, 8 * g->num_sms), 256, 0, g->stream>>>(
+            acc_final, n, B, cfg.b_valid, cfg.stranger, cfg.scale, cfg.node_major ? 1 : 0, cfg.out);
+        CKL("k_combine");
+        ++g->launches;
+    }
+    if (res && cfg.want_state) {
+        res->state.resize(B);
+        CK(cudaMemcpyAsync(res->state.data(), st + (done & 1) * B, B * sizeof(ColState),
+                           cudaMemcpyDeviceToHost, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+    }
+}
+
+static void upload(tpa_graph* g, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g->stream));
+}
+static void download(tpa_graph* g, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g->stream));
+}
+static void finish(tpa_graph* g, int flags) {
+    if (!((flags & TPA_DEVICE_PTRS) && (flags & TPA_ASYNC))) CK(cudaStreamSynchronize(g->stream));
+}
+
+static int batch_width(uint32_t b) {
+    if (b <= 1) return 1;
+    if (b <= 8) return 8;
+    if (b <= 16) return 16;
+    if (b <= 32) return 32;
+    return 64;
+}
+
+// Batched single-seed runs over seeds[0..B): query / query_na / exact_rwr.
+// `seeds` is a host array; `out` is host or device per flags.
+static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, double c, double eps,
+                           uint32_t start, int64_t terminal, const double* stranger, double scale,
+                           bool combine, double* out, int flags) {
+    const bool dev = flags & TPA_DEVICE_PTRS;
+    const bool node_major = flags & TPA_NODE_MAJOR;
+    const uint32_t n = g->n;
+    std::vector<uint32_t> hseeds(seeds, seeds + Btot);  // host copy (callers resolve device lists)
+    for (uint32_t b = 0; b < Btot; ++b) validate_seed(hseeds[b], n);
+    if (node_major && Btot != (uint32_t)batch_width(Btot))
+        throw std::invalid_argument("node-major output needs B in {8, 16, 32, 64}");
+    if (node_major && Btot == 1)
+        throw std::invalid_argument("node-major output needs B in {8, 16, 32, 64}");
+    DevBuf& stage = g->out_stage;
+    if (!dev) stage.ensure((size_t)std::min<uint32_t>(Btot, 64) * n * sizeof(double), g->stream);
+    for (uint32_t b0 = 0; b0 < Btot; b0 += 64) {
+        const uint32_t bv = std::min<uint32_t>(64, Btot - b0);
+        const int B = batch_width(bv);
+        Workspace& w = g->workspace(B);
+        (void)w;
+        RunCfg cfg;
+        cfg.B = B;
+        cfg.b_valid = bv;
+        cfg.c = c;
+        cfg.eps = eps;
+        cfg.start = start;
+        cfg.terminal = terminal;
+        cfg.want_state = false;
+        if (B == 1) {
+            // single seed through the SpMV path: dense x⁽⁰⁾ = c·e_seed
+            cfg.init = Init::Seeds;
+        } else {
+            cfg.init = Init::Seeds;
+        }
+        for (uint32_t b = 0; b < bv; ++b) cfg.seeds.s[b] = hseeds[b0 + b];
+        cfg.acc = w.acc.as<double>();
+        double* dst = dev ? out + (node_major ? 0 : (size_t)b0 * n) : stage.as<double>();
+        if (combine) {
+            cfg.out = dst;
+            cfg.stranger = stranger;
+            cfg.scale = scale;
+            cfg.node_major = node_major;
+        }
+        RunOut ro;
+        run_cpi(g, cfg, &ro);
+        if (!combine) {
+            // exact_rwr: the accumulator is the answer
+            if (node_major) {
+                CK(cudaMemcpyAsync(dst, w.acc.p, (size_t)n * B * 8, cudaMemcpyDeviceToDevice, g->stream));
+            } else if (B == 1) {
+                CK(cudaMemcpyAsync(dst, w.acc.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, g->stream));
+            } else {
+                k_transpose<<<grid_for((uint64_t)n * B, 256, 8 * g->num_sms), 256, 0, g->stream>>>(
+                    w.acc.as<double>(), n, B, bv, dst);
+                CKL("k_transpose");
+                ++g->launches;
+            }
+        }
+        if (!dev) download(g, out + (size_t)b0 * n, stage.p, (size_t)bv * n * 8);
+    }
+    finish(g, flags);
+}
+
+}  // namespace tpa
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int tpa_abi_version(void) { return TPA_ABI_VERSION; }
+const char* tpa_last_error(void) { return tpa::last_error().c_str(); }
+
+int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
+                     const uint32_t* out_targets, int policy, uint64_t fingerprint, int device,
+                     tpa_graph** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output handle");
+        if (n == 0) throw std::invalid_argument("graph must have at least one node");
+        if (policy < 0 || policy > 2) throw std::invalid_argument("unknown dangling policy");
+        if (out_offsets[n] != m) throw std::invalid_argument("out_offsets[n] != m");
+        DeviceGuard dg(device);
+        {
+            const cudaError_t stale = cudaGetLastError();
+            if (stale != cudaSuccess && std::getenv("TPA_DEBUG"))
+                fprintf(stderr, "tpa: stale CUDA error before graph create: %s\n", cudaGetErrorString(stale));
+        }
+        auto g = std::make_unique<tpa_graph>();
+        g->device = device;
+        g->n = n;
+        g->m = m;
+        g->policy = policy;
+        g->fingerprint = fingerprint;
+        CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        g->own_stream = true;
+        cudaStream_t s = g->stream;
+        {
+            // keep freed blocks in the device pool (no release at sync points)
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t thr = UINT64_MAX;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
+
+        DevBuf d_off, d_tgt, d_src, d_keys;
+        d_off.ensure((n + 1ull) * 8, g->stream);
+        d_tgt.ensure(m * 4, g->stream);
+        d_src.ensure(m * 4, g->stream);
+        d_keys.ensure(m * 4, g->stream);
+        g->col.ensure(m * 4, g->stream);
+        g->deg.ensure((size_t)n * 4, g->stream);
+        g->row_ptr.ensure((n + 1ull) * 8, g->stream);
+        CK(cudaMemcpyAsync(d_off.p, out_offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
+        if (m) CK(cudaMemcpyAsync(d_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
+        const int blocks = 8 * g->num_sms;
+        k_degrees<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>(), n, g->deg.as<uint32_t>());
+        k_expand_src<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>(), n, d_src.as<uint32_t>());
+        CKL("k_expand_src");
+        int end_bit = 1;
+        while (end_bit < 32 && ((uint64_t)1 << end_bit) < n) ++end_bit;
+        if (m) {
+            size_t temp = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, d_tgt.as<uint32_t>(), d_keys.as<uint32_t>(),
+                                               d_src.as<uint32_t>(), g->col.as<uint32_t>(), (int64_t)m, 0,
+                                               end_bit, s));
+            DevBuf d_temp;
+            d_temp.ensure(temp, g->stream);
+            CK(cub::DeviceRadixSort::SortPairs(d_temp.p, temp, d_tgt.as<uint32_t>(), d_keys.as<uint32_t>(),
+                                               d_src.as<uint32_t>(), g->col.as<uint32_t>(), (int64_t)m, 0,
+                                               end_bit, s));
+        }
+        k_row_ptr<<<blocks, 256, 0, s>>>(d_keys.as<uint32_t>(), m, n, g->row_ptr.as<int64_t>());
+        CKL("k_row_ptr");
+        std::vector<int64_t> rp(n + 1ull);
+        CK(cudaMemcpyAsync(rp.data(), g->row_ptr.p, (n + 1ull) * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        g->launches += 4;
+
+        auto mv = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
+        auto mm = build_items(rp, n, kMmTileNnz, kMmTileRows, kMmLongRow);
+        for (auto* pr : {&mv, &mm})
+            if (pr->size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
+        g->mv.n_items = (uint32_t)mv.size();
+        g->mv.n_groups = (g->mv.n_items + kGroupItems - 1) / kGroupItems;
+        g->mv.items.ensure(mv.size() * sizeof(uint2), g->stream);
+        CK(cudaMemcpyAsync(g->mv.items.p, mv.data(), mv.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+        g->mm.n_items = (uint32_t)mm.size();
+        g->mm.n_groups = (g->mm.n_items + kGroupItems - 1) / kGroupItems;
+        g->mm.items.ensure(mm.size() * sizeof(uint2), g->stream);
+        CK(cudaMemcpyAsync(g->mm.items.p, mm.data(), mm.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        *out = g.release();
+    });
+}
+
+int tpa_graph_destroy(tpa_graph* g) {
+    return guard([&] {
+        if (!g) return;
+        {
+            DeviceGuard dg(g->device);
+            // stream-ordered frees first, then drain and drop the stream
+            g->ws.clear();
+            g->row_ptr.release();
+            g->col.release();
+            g->deg.release();
+            g->mv.items.release();
+            g->mm.items.release();
+            g->init_part.release();
+            g->out_stage.release();
+            for (tpa_artifact* a : g->artifacts) detach_artifact(a);
+            g->artifacts.clear();
+            cudaStreamSynchronize(g->stream);
+            for (auto& pe : g->prof_events) {
+                cudaEventDestroy(pe.second.first);
+                cudaEventDestroy(pe.second.second);
+            }
+            for (auto e : g->event_pool) cudaEventDestroy(e);
+            if (g->own_stream) cudaStreamDestroy(g->stream);
+        }
+        delete g;
+    });
+}
+
+int tpa_graph_set_stream(tpa_graph* g, void* cuda_stream) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        CK(cudaStreamSynchronize(g->stream));
+        if (g->own_stream) cudaStreamDestroy(g->stream);
+        if (cuda_stream) {
+            g->stream = static_cast<cudaStream_t>(cuda_stream);
+            g->own_stream = false;
+        } else {
+            CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+            g->own_stream = true;
+        }
+    });
+}
+
+int tpa_graph_info(const tpa_graph* g, uint32_t* n, uint64_t* m, uint64_t* fingerprint, int* policy,
+                   uint64_t* device_bytes) {
+    return guard([&] {
+        if (n) *n = g->n;
+        if (m) *m = g->m;
+        if (fingerprint) *fingerprint = g->fingerprint;
+        if (policy) *policy = g->policy;
+        if (device_bytes) {
+            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->mm.items.bytes;
+            for (auto& kv : g->ws) {
+                const Workspace& w = *kv.second;
+                b += w.share[0].bytes + w.share[1].bytes + w.acc.bytes + w.part.bytes + w.gpart.bytes;
+            }
+            *device_bytes = b;
+        }
+    });
+}
+
+uint64_t tpa_graph_launches(const tpa_graph* g) { return g ? g->launches : 0; }
+
+int tpa_graph_profile(tpa_graph* g, int enable) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        if (enable) {
+            CK(cudaStreamSynchronize(g->stream));
+            for (auto& pe : g->prof_events) {
+                g->event_pool.push_back(pe.second.first);
+                g->event_pool.push_back(pe.second.second);
+            }
+            g->prof_events.clear();
+        }
+        g->profile = enable != 0;
+    });
+}
+
+int tpa_graph_profile_read(tpa_graph* g, int width, uint64_t* launches, double* total_ms) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        CK(cudaStreamSynchronize(g->stream));
+        uint64_t cnt = 0;
+        double tot = 0.0;
+        for (auto& pe : g->prof_events) {
+            if (pe.first != width) continue;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
+            tot += ms;
+            ++cnt;
+        }
+        if (launches) *launches = cnt;
+        if (total_ms) *total_ms = tot;
+    });
+}
+
+int tpa_graph_transpose(const tpa_graph* g, int64_t* row_ptr, uint32_t* col) {
+    return guard([&] {
+        DeviceGuard dg(g->device);
+        if (row_ptr) CK(cudaMemcpy(row_ptr, g->row_ptr.p, (g->n + 1ull) * 8, cudaMemcpyDeviceToHost));
+        if (col && g->m) CK(cudaMemcpy(col, g->col.p, g->m * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int tpa_propagation_sweep(tpa_graph* g, const double* x, double* y, double c, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        // graph.cpp:233-235
+        if (c < 0.0 || c >= 1.0) throw std::invalid_argument("restart probability must be in [0, 1)");
+        const bool dev = flags & TPA_DEVICE_PTRS;
+        const size_t nb = (size_t)g->n * 8;
+        DevBuf dx, dy;
+        const double* xd = x;
+        double* yd = y;
+        if (!dev) {
+            dx.ensure(nb, g->stream);
+            dy.ensure(nb, g->stream);
+            upload(g, dx.p, x, nb);
+            xd = dx.as<double>();
+            yd = dy.as<double>();
+        }
+        RunCfg cfg;
+        cfg.B = 1;
+        cfg.c = c;
+        cfg.eps = 1.0;  // no convergence semantics for a single sweep
+        cfg.terminal = 1;
+        cfg.init = Init::Dense;
+        cfg.d_x = xd;
+        cfg.y_out = yd;
+        cfg.want_state = false;
+        // c == 0 is legal for a sweep; the driver only uses keep = 1 - c.
+        run_cpi(g, cfg, nullptr);
+        if (!dev) download(g, y, yd, nb);
+        finish(g, flags);
+    });
+}
+
+int tpa_cpi_run(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, double c, double eps,
+                uint32_t start_iter, int64_t terminal_iter, double* out_scores,
+                uint32_t* iterations_run, int* converged, double* residual_l1, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        const bool dev = flags & TPA_DEVICE_PTRS;
+        std::vector<uint32_t> hs;
+        if (seeds) {
+            // SeedSet (cpi.cpp:19-24): non-empty, sorted, duplicate-free
+            if (n_seeds == 0) throw std::invalid_argument("seed set must not be empty");
+            hs.resize(n_seeds);
+            if (dev) CK(cudaMemcpy(hs.data(), seeds, n_seeds * 4, cudaMemcpyDeviceToHost));
+            else std::memcpy(hs.data(), seeds, n_seeds * 4);
+            std::sort(hs.begin(), hs.end());
+            if (std::adjacent_find(hs.begin(), hs.end()) != hs.end())
+                throw std::invalid_argument("seed set contains duplicate ids");
+        }
+        validate_cpi(c, eps, start_iter, terminal_iter);
+        if (seeds) validate_seed(hs.back(), g->n);
+        const uint32_t n = g->n;
+        Workspace& w = g->workspace(1);
+        RunCfg cfg;
+        cfg.B = 1;
+        cfg.c = c;
+        cfg.eps = eps;
+        cfg.start = start_iter;
+        cfg.terminal = terminal_iter;
+        cfg.acc = dev ? out_scores : w.acc.as<double>();
+        DevBuf dx;
+        if (!seeds) {
+            cfg.init = Init::Dense;
+            cfg.weight = c / (double)n;  // cpi.cpp:61
+        } else if (hs.size() == 1) {
+            cfg.init = Init::Seeds;
+            cfg.seeds.s[0] = hs[0];
+        } else {
+            std::vector<double> x0(n, 0.0);
+            const double wgt = c / (double)hs.size();
+            for (uint32_t s : hs) x0[s] = wgt;
+            dx.ensure((size_t)n * 8, g->stream);
+            upload(g, dx.p, x0.data(), (size_t)n * 8);
+            cfg.init = Init::Dense;
+            cfg.d_x = dx.as<double>();
+            CK(cudaStreamSynchronize(g->stream));
+        }
+        RunOut ro;
+        run_cpi(g, cfg, &ro);
+        if (!dev) download(g, out_scores, cfg.acc, (size_t)n * 8);
+        CK(cudaStreamSynchronize(g->stream));
+        if (iterations_run) *iterations_run = ro.state[0].iters;
+        if (converged) *converged = ro.state[0].converged;
+        if (residual_l1) *residual_l1 = ro.state[0].residual;
+    });
+}
+
+int tpa_cpi_partition(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, double c, double eps,
+                      const uint32_t* boundaries, uint64_t n_boundaries, double* out, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        const bool dev = flags & TPA_DEVICE_PTRS;
+        // cpi.cpp:117-125
+        std::vector<uint32_t> hs;
+        if (seeds == nullptr || n_seeds == 0) throw std::invalid_argument("seed set must not be empty");
+        hs.assign(seeds, seeds + n_seeds);
+        std::sort(hs.begin(), hs.end());
+        if (std::adjacent_find(hs.begin(), hs.end()) != hs.end())
+            throw std::invalid_argument("seed set contains duplicate ids");
+        validate_cpi(c, eps, 0, -1);
+        std::vector<uint32_t> bounds(boundaries, boundaries + n_boundaries);
+        for (size_t k = 0; k < bounds.size(); ++k) {
+            const uint32_t lo = k == 0 ? 1 : bounds[k - 1] + 1;
+            if (bounds[k] < lo)
+                throw std::invalid_argument("partition boundaries must be strictly increasing and >= 1");
+        }
+        validate_seed(hs.back(), g->n);
+        const uint32_t n = g->n;
+        const size_t nseg = bounds.size() + 1;
+        DevBuf segs, dx;
+        double* base = out;
+        if (!dev) {
+            segs.ensure(nseg * n * 8, g->stream);
+            base = segs.as<double>();
+        }
+        RunCfg cfg;
+        cfg.B = 1;
+        cfg.c = c;
+        cfg.eps = eps;
+        cfg.bounds = bounds;
+        for (size_t k = 0; k < nseg; ++k) cfg.seg_acc.push_back(base + k * n);
+        Workspace& w = g->workspace(1);
+        if (hs.size() == 1) {
+            cfg.init = Init::Seeds;
+            cfg.seeds.s[0] = hs[0];
+        } else {
+            std::vector<double> x0(n, 0.0);
+            const double wgt = c / (double)hs.size();
+            for (uint32_t s : hs) x0[s] = wgt;
+            dx.ensure((size_t)n * 8, g->stream);
+            upload(g, dx.p, x0.data(), (size_t)n * 8);
+            cfg.init = Init::Dense;
+            cfg.d_x = dx.as<double>();
+            CK(cudaStreamSynchronize(g->stream));
+        }
+        RunOut ro;
+        run_cpi(g, cfg, &ro);
+        if (!dev) download(g, out, base, nseg * n * 8);
+        finish(g, flags);
+    });
+}
+
+int tpa_exact_rwr_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, double c, double eps,
+                        double* out, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        if (B == 0) throw std::invalid_argument("seed set must not be empty");
+        validate_cpi(c, eps, 0, -1);
+        run_seed_batch(g, seeds, B, c, eps, 0, -1, nullptr, 1.0, false, out, flags);
+    });
+}
+
+double tpa_neighbor_scale_factor(double c, uint32_t S, uint32_t T) {
+    // tpa.cpp:39-44 -- host std::pow, exactly as the reference.
+    const double keep = 1.0 - c;
+    const double family_mass = 1.0 - std::pow(keep, S);
+    const double neighbor_mass = std::pow(keep, S) - std::pow(keep, T);
+    return neighbor_mass / family_mass;
+}
+
+int tpa_preprocess(tpa_graph* g, double c, double eps, uint32_t T, double* out_stranger,
+                   tpa_artifact** out_artifact, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        if (T < 1) throw std::invalid_argument("stranger_start (T) must be at least 1");  // tpa.cpp:21-22
+        validate_cpi(c, eps, T, -1);
+        const bool dev = flags & TPA_DEVICE_PTRS;
+        auto art = std::make_unique<tpa_artifact>();
+        art->g = g;
+        art->fingerprint = g->fingerprint;
+        art->c = c;
+        art->eps = eps;
+        art->T = T;
+        art->stranger.ensure((size_t)g->n * 8, g->stream);
+        RunCfg cfg;
+        cfg.B = 1;
+        cfg.c = c;
+        cfg.eps = eps;
+        cfg.start = T;
+        cfg.terminal = -1;
+        cfg.init = Init::Dense;
+        cfg.weight = c / (double)g->n;
+        cfg.acc = art->stranger.as<double>();
+        cfg.want_state = false;
+        run_cpi(g, cfg, nullptr);
+        if (out_stranger) {
+            if (dev)
+                CK(cudaMemcpyAsync(out_stranger, art->stranger.p, (size_t)g->n * 8, cudaMemcpyDeviceToDevice,
+                                   g->stream));
+            else
+                download(g, out_stranger, art->stranger.p, (size_t)g->n * 8);
+        }
+        finish(g, flags);
+        if (out_artifact) {
+            g->artifacts.insert(art.get());
+            *out_artifact = art.release();
+        }
+    });
+}
+
+int tpa_artifact_create(tpa_graph* g, const double* stranger, uint64_t graph_fingerprint, double c,
+                        double eps, uint32_t T, int flags, tpa_artifact** out) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        auto art = std::make_unique<tpa_artifact>();
+        art->g = g;
+        art->fingerprint = graph_fingerprint;
+        art->c = c;
+        art->eps = eps;
+        art->T = T;
+        art->stranger.ensure((size_t)g->n * 8, g->stream);
+        CK(cudaMemcpyAsync(art->stranger.p, stranger, (size_t)g->n * 8,
+                           (flags & TPA_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+        g->artifacts.insert(art.get());
+        *out = art.release();
+    });
+}
+
+int tpa_artifact_destroy(tpa_artifact* a) {
+    return guard([&] {
+        if (!a) return;
+        if (tpa_graph* g = a->g) {
+            std::lock_guard<std::mutex> lk(g->mu);
+            DeviceGuard dg(g->device);
+            g->artifacts.erase(a);
+            a->stranger.release();
+        }
+        delete a;
+    });
+}
+
+static void check_query(tpa_graph* g, const tpa_artifact* a, uint32_t S) {
+    // tpa.cpp:63-66, then cpi_run's CpiParams::validate with the artifact's c/eps (tpa.cpp:69)
+    if (a->fingerprint != g->fingerprint)
+        throw std::runtime_error("stale artifact: graph fingerprint mismatch");
+    if (a->g == nullptr) throw std::runtime_error("artifact outlived its graph handle");
+    if (a->g->device != g->device) throw std::invalid_argument("artifact lives on another device");
+    if (S < 1 || S >= a->T) throw std::invalid_argument("family_end (S) must satisfy 1 <= S < T");
+    validate_cpi(a->c, a->eps, 0, (int64_t)S - 1);
+}
+
+int tpa_query(tpa_graph* g, const tpa_artifact* a, uint32_t seed, uint32_t S, double* out, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        if (!a) throw std::invalid_argument("null artifact");
+        check_query(g, a, S);
+        const double scale = 1.0 + tpa_neighbor_scale_factor(a->c, S, a->T);
+        run_seed_batch(g, &seed, 1, a->c, a->eps, 0, (int64_t)S - 1, a->stranger.as<double>(), scale, true,
+                       out, flags);
+    });
+}
+
+int tpa_query_batch(tpa_graph* g, const tpa_artifact* a, const uint32_t* seeds, uint32_t B, uint32_t S,
+                    double* out, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        if (!a) throw std::invalid_argument("null artifact");
+        check_query(g, a, S);
+        if (B == 0) return;
+        const bool na = flags & TPA_QUERY_NA;
+        const double scale = 1.0 + tpa_neighbor_scale_factor(a->c, S, a->T);  // tpa.cpp:71-72
+        run_seed_batch(g, seeds, B, a->c, a->eps, 0, (int64_t)S - 1, na ? nullptr : a->stranger.as<double>(),
+                       scale, true, out, flags);
+    });
+}
+
+int tpa_query_na_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, uint32_t S, uint32_t T, double c,
+                       double eps, double* out, int flags) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(g->mu);
+        DeviceGuard dg(g->device);
+        // TpaParams::validate (tpa.cpp:8-17)
+        if (S < 1) throw std::invalid_argument("family_end (S) must be at least 1");
+        if (T <= S) throw std::invalid_argument("stranger_start (T) must exceed family_end (S)");
+        validate_cpi(c, eps, 0, -1);
+        if (B == 0) return;
+        const double scale = 1.0 + tpa_neighbor_scale_factor(c, S, T);
+        run_seed_batch(g, seeds, B, c, eps, 0, (int64_t)S - 1, nullptr, scale, true, out, flags);
+    });
+}
+
+}  // extern "C"
