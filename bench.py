@@ -279,7 +279,10 @@ def run_ours(args):
     dg = g.device(local)
     torch.cuda.synchronize()
     t_ingest = time.perf_counter() - t0
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) torch stream: the library enqueues on it, so the
+    # torch events below bracket exactly the library's kernels
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     dg.set_stream(stream.cuda_stream)
     lib = N.lib
     h = dg.h

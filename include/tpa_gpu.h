@@ -21,10 +21,13 @@
  * vectors (tpa_test.cpp:148-161).  The reference's `threads` argument selects
  * host parallelism; here it has no meaning and is not taken.
  *
- * Memory: unless TPA_DEVICE_PTRS is set, vector arguments are host pointers
- * (pinned or pageable).  With TPA_DEVICE_PTRS they are device pointers on the
- * handle's device and the call returns without a host synchronisation when
- * nothing has to come back to the host (TPA_ASYNC).
+ * Memory: unless TPA_DEVICE_PTRS is set, vector (double) arguments are host
+ * pointers (pinned or pageable).  With TPA_DEVICE_PTRS they are device
+ * pointers on the handle's device and the call returns without a host
+ * synchronisation when nothing has to come back to the host (TPA_ASYNC).
+ * Seed and boundary lists are ALWAYS host arrays: they are validated on the
+ * host before any launch (the reference's error order) and travel to the
+ * device as kernel parameters.
  */
 #ifndef TPA_GPU_H
 #define TPA_GPU_H

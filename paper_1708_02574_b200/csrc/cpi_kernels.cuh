@@ -44,11 +44,6 @@ constexpr int kGroupItems = 128;      // items per first-level ticket group
 constexpr int kMvTileNnz = 2048;      // gathered values staged in smem per CTA
 constexpr int kMvTileRows = 512;
 constexpr int kMvShortRow = 32;       // rows <= this: one thread, sequential
-// SpMM (B >= 8) tiling.
-constexpr int kMmTileNnz = 2048;
-constexpr int kMmTileRows = 256;
-constexpr int kMmLongRow = 4096;      // rows above: CTA item, 8 ordered chunks
-constexpr int kMmChunks = 8;
 
 // Per-column CPI state, double-buffered by sweep parity.
 struct ColState {
@@ -359,10 +354,8 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv(StepArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: fused CPI sweep, B seeds at once (B in {8,16,32,64}); iterate row-major
-// n x B so a gather of source u reads B*8 contiguous bytes.  G = min(B,32)
-// lanes per row, CPL = B/G columns per lane.  Lane = column, so each column's
-// row sum is a plain sequential ascending-source chain.
+// K3 (SpMM, B in {8,16,32,64}) lives in cpi_spmm.cuh.  Shape helpers: G =
+// min(B,32) lanes per row, CPL = B/G columns per lane.
 // ---------------------------------------------------------------------------
 template <int B>
 struct MmVec;
@@ -380,193 +373,6 @@ __device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
         v[0] = t.x;
         v[1] = t.y;
     }
-}
-
-template <int B>
-__global__ void __launch_bounds__(kThreads) k_step_spmm(StepArgs a) {
-    constexpr int G = MmVec<B>::G, CPL = MmVec<B>::CPL;
-    constexpr int NGRP = kThreads / G;
-    constexpr int U = 8;  // gathers in flight per lane
-    __shared__ double s_red[kThreads * 2 * CPL];  // (l1 | dm) x NGRP x B
-    __shared__ double s_fin[kThreads];
-    __shared__ double s_part[2 * B];
-    __shared__ double s_chunk[kMmChunks][B];
-    __shared__ ColState s_st[B];
-    __shared__ int s_any;
-
-    const int tid = threadIdx.x;
-    const int grp = tid / G, gl = tid % G;
-    const uint32_t item = blockIdx.x;
-    const uint2 it = a.items[item];
-    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
-    const bool is_long = (it.y & kLongFlag) != 0;
-
-    if (tid == 0) s_any = 0;
-    __syncthreads();
-    for (int b = tid; b < B; b += kThreads) {
-        s_st[b] = a.state_in[b];
-        if (s_st[b].active) s_any = 1;
-    }
-    __syncthreads();
-    if (!s_any) {
-        if (a.out)
-            for (uint32_t v = rb + tid / B; v < re; v += kThreads / B) {
-                const uint32_t b = tid % B;
-                combine_only(a, v, b, B, (size_t)v * B + b);
-            }
-        if (item == 0)
-            for (int b = tid; b < B; b += kThreads) a.state_out[b] = s_st[b];
-        return;
-    }
-
-    const int c0 = gl * CPL;  // first column of this lane
-    ColState my_st[CPL];
-    bool act[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-        my_st[c] = s_st[c0 + c];
-        act[c] = my_st[c].active != 0;
-    }
-    const bool want_dm = a.policy == kUniform;
-    double my_l1[CPL], my_dm[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) my_l1[c] = my_dm[c] = 0.0;
-
-    if (!is_long) {
-        // Groups of one warp stay in lock-step: the trip count is the warp max.
-        constexpr int GPW = 32 / G;  // groups (rows) per warp
-        const int warp = tid >> 5;
-        for (uint32_t base = rb + warp * GPW; base < re; base += NGRP) {
-            const uint32_t r = base + (grp % GPW);
-            const bool has_row = r < re;
-            int64_t lo = 0, hi = 0;
-            if (has_row) {
-                lo = __ldg(a.row_ptr + r);
-                hi = __ldg(a.row_ptr + r + 1);
-            }
-            const int len = (int)(hi - lo);
-            int maxlen = len;
-            if constexpr (GPW > 1) maxlen = __reduce_max_sync(0xffffffffu, len);
-            double s[CPL];
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) s[c] = 0.0;
-            for (int off = 0; off < maxlen; off += G) {
-                const int cnt = min(G, len - off);  // may be <= 0 for this group
-                const uint32_t myidx = gl < cnt ? ld_stream_u32(a.col + lo + off + gl) : 0u;
-                for (int j0 = 0; j0 < G; j0 += U) {
-                    if (j0 >= (maxlen - off)) break;  // warp-uniform
-                    double v[U][CPL];
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const uint32_t u = __shfl_sync(0xffffffffu, myidx, j0 + j, G);
-                        if (j0 + j < cnt) {
-                            ld_cols<CPL>(a.share_in + (size_t)u * B + c0, v[j]);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < U; ++j)
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
-                }
-            }
-            if (has_row) {
-                const uint32_t d = __ldg(a.deg + r);
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const size_t idx = (size_t)r * B + c0 + c;
-                    if (act[c]) {
-                        const double y = epilogue(a, my_st[c], r, c0 + c, B, idx, s[c], d);
-                        my_l1[c] = dadd(my_l1[c], y);
-                        if (want_dm && d == 0) my_dm[c] = dadd(my_dm[c], y);
-                    } else {
-                        combine_only(a, r, c0 + c, B, idx);
-                    }
-                }
-            }
-        }
-    } else {
-        // Long row: kMmChunks fixed chunks (function of the row length only),
-        // each summed sequentially by one group, then combined in chunk order.
-        const int64_t lo = __ldg(a.row_ptr + rb), hi = __ldg(a.row_ptr + rb + 1);
-        const int64_t len = hi - lo;
-        if (grp < kMmChunks) {
-            const int64_t c_lo = lo + len * grp / kMmChunks;
-            const int64_t c_hi = lo + len * (grp + 1) / kMmChunks;
-            double s[CPL];
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) s[c] = 0.0;
-            for (int64_t off = c_lo; off < c_hi; off += G) {
-                const int cnt = (int)min((int64_t)G, c_hi - off);
-                const uint32_t myidx = gl < cnt ? ld_stream_u32(a.col + off + gl) : 0u;
-                for (int j0 = 0; j0 < cnt; j0 += U) {
-                    double v[U][CPL];
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const uint32_t u = __shfl_sync(0xffffffffu >> (32 - G) << ((tid & 31) / G * G),
-                                                       myidx, j0 + j, G);
-                        if (j0 + j < cnt) {
-                            ld_cols<CPL>(a.share_in + (size_t)u * B + c0, v[j]);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < U; ++j)
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) s_chunk[grp][c0 + c] = s[c];
-        }
-        __syncthreads();
-        if (tid < B) {
-            double y = s_chunk[0][tid];
-#pragma unroll
-            for (int k = 1; k < kMmChunks; ++k) y = dadd(y, s_chunk[k][tid]);
-            s_chunk[0][tid] = y;
-        }
-        __syncthreads();
-        // Epilogue by the lanes of group 0 so the per-lane partial layout holds.
-        if (grp == 0) {
-            const uint32_t d = __ldg(a.deg + rb);
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-                const size_t idx = (size_t)rb * B + c0 + c;
-                if (act[c]) {
-                    const double y = epilogue(a, my_st[c], rb, c0 + c, B, idx, s_chunk[0][c0 + c], d);
-                    my_l1[c] = y;
-                    if (want_dm && d == 0) my_dm[c] = y;
-                } else {
-                    combine_only(a, rb, c0 + c, B, idx);
-                }
-            }
-        }
-    }
-    // Per-column partials: groups in fixed order (tree over groups).
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-        s_red[grp * B + c0 + c] = my_l1[c];
-        s_red[NGRP * B + grp * B + c0 + c] = my_dm[c];
-    }
-    __syncthreads();
-    for (int w = NGRP / 2; w > 0; w >>= 1) {
-        for (int t = tid; t < w * B; t += kThreads) {
-            s_red[t] = dadd(s_red[t], s_red[t + w * B]);
-            s_red[NGRP * B + t] = dadd(s_red[NGRP * B + t], s_red[NGRP * B + t + w * B]);
-        }
-        __syncthreads();
-    }
-    for (int b = tid; b < B; b += kThreads) {
-        s_part[b] = s_red[b];
-        s_part[B + b] = s_red[NGRP * B + b];
-    }
-    __syncthreads();
-    finish_item(a, item, B, s_part, s_red, s_fin);
 }
 
 }  // namespace tpa

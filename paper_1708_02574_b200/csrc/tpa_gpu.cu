@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "cpi_kernels.cuh"
+#include "cpi_spmm.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
 
@@ -208,29 +209,74 @@ __global__ void k_init_seeds(const SeedList seeds, uint32_t b_valid, int B, doub
     state0[b] = s;
 }
 
+// SpMM batches: x⁽⁰⁾ rows of the seeds only.  Each seed's thread writes the
+// seed's whole B-wide row of share0 / acc0 (identical data when two columns
+// share a seed) and marks it in the frontier and acc_valid bitmaps; nothing
+// else is zero-filled (cpi.cpp:59-63).
+__global__ void k_init_seeds_mm(const SeedList seeds, uint32_t b_valid, int B, double c, double keep,
+                                uint32_t n, int policy, const uint32_t* __restrict__ deg,
+                                double* __restrict__ share0, double* __restrict__ acc0,
+                                uint32_t* __restrict__ nz0, uint32_t* __restrict__ acc_valid, int active0,
+                                ColState* state0) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    ColState s;
+    s.iters = 0;
+    s.converged = 0;
+    if (b < (int)b_valid) {
+        const uint32_t seed = seeds.s[b];
+        const uint32_t d = deg[seed];
+        const double w = c;  // c / |S|, |S| = 1
+        const double sh = d ? ddiv(dmul(keep, w), (double)d) : 0.0;
+        for (int k = 0; k < B; ++k) {
+            const bool mine = k < (int)b_valid && seeds.s[k] == seed;
+            share0[(size_t)seed * B + k] = mine ? sh : 0.0;
+            if (acc0) acc0[(size_t)seed * B + k] = mine ? w : 0.0;
+        }
+        atomicOr(nz0 + (seed >> 5), 1u << (seed & 31));
+        if (acc0) atomicOr(acc_valid + (seed >> 5), 1u << (seed & 31));
+        s.residual = w;
+        s.active = active0;
+        s.has_spread = policy == kUniform && d == 0;
+        s.spread = s.has_spread ? ddiv(dmul(keep, w), (double)n) : 0.0;
+    } else {
+        s.residual = 0.0;
+        s.active = 0;
+        s.has_spread = 0;
+        s.spread = 0.0;
+    }
+    state0[b] = s;
+}
+
+__device__ __forceinline__ bool row_valid(const uint32_t* acc_valid, uint32_t v) {
+    return !acc_valid || ((__ldg(acc_valid + (v >> 5)) >> (v & 31)) & 1u);
+}
+
 // K5 standalone combine (S = 1, or every column stopped before sweep S-1).
-__global__ void k_combine(const double* __restrict__ acc, uint32_t n, int B, uint32_t b_valid,
-                          const double* __restrict__ stranger, double scale, int node_major,
-                          double* __restrict__ out) {
+__global__ void k_combine(const double* __restrict__ acc, const uint32_t* __restrict__ acc_valid,
+                          uint32_t n, int B, uint32_t b_valid, const double* __restrict__ stranger,
+                          double scale, int node_major, double* __restrict__ out) {
     const uint64_t total = (uint64_t)n * B;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(i / B), b = (uint32_t)(i % B);
         if (b >= b_valid) continue;
-        const double f = acc[i];
+        const double f = row_valid(acc_valid, v) ? acc[i] : 0.0;
         const size_t o = node_major ? i : (size_t)b * n + v;
         out[o] = stranger ? dadd(dmul(scale, f), stranger[v]) : dmul(f, scale);
     }
 }
 
-// [n][B] -> [B][n] for the first b_valid columns.
-__global__ void k_transpose(const double* __restrict__ src, uint32_t n, int B, uint32_t b_valid,
-                            double* __restrict__ dst) {
+// acc [n][B] (rows outside acc_valid are zero) -> [B][n] or [n][B].
+__global__ void k_acc_export(const double* __restrict__ src, const uint32_t* __restrict__ acc_valid,
+                             uint32_t n, int B, uint32_t b_valid, int node_major, double* __restrict__ dst) {
     const uint64_t total = (uint64_t)n * B;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(i / B), b = (uint32_t)(i % B);
-        if (b < b_valid) dst[(size_t)b * n + v] = src[i];
+        if (b >= b_valid) continue;
+        const double x = row_valid(acc_valid, v) ? src[i] : 0.0;
+        dst[node_major ? i : (size_t)b * n + v] = x;
     }
 }
 
@@ -277,9 +323,30 @@ std::vector<uint2> build_items(const std::vector<int64_t>& rp, uint32_t n, int64
     return items;
 }
 
+// Persistent-grid sizing for k_step_spmm2<B> (dynamic smem = the row-sum buffers).
+template <int B>
+static int mm_occupancy() {
+    const size_t dyn = MmShape<B>::kDynSmem;
+    CK(cudaFuncSetAttribute(k_step_spmm2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmm2<B>, MmShape<B>::NT, dyn));
+    return occ;
+}
+
 struct Workspace {
     int B = 0;
     DevBuf share[2], acc, part, gpart, group_cnt, done_cnt, state;
+    // SpMM (B > 1) extras
+    DevBuf nz[2], acc_valid, long_cnt, seg_part, work_cnt, fx;
+    int grid = 0;  // persistent grid of k_step_spmm2<B>
+};
+
+// Long rows of CSR(Ãᵀ) (in-degree > kLong) cut into kLong-nnz segments, the
+// SpMM's first work items (longest rows first).
+struct LongRows {
+    DevBuf seg_row, seg_lo, seg_long, long_first, long_nseg;
+    uint32_t n_segs = 0, n_long = 0;
+    DevBuf blocks;  // short-row blocks {first row, rows}
 };
 
 }  // namespace tpa
@@ -295,7 +362,9 @@ struct tpa_graph {
     int policy = 0;
     uint64_t fingerprint = 0;
     DevBuf row_ptr, col, deg;
-    Schedule mv, mm;
+    Schedule mv;  // SpMV work items
+    LongRows longs;
+    uint32_t n_blocks = 0;  // kMmRows-row blocks
     std::map<int, std::unique_ptr<Workspace>> ws;
     DevBuf init_part;
     DevBuf out_stage;  // host-output staging for batch calls
@@ -325,20 +394,50 @@ struct tpa_graph {
             p->B = B;
         }
         Workspace& w = *p;
-        const Schedule& s = B == 1 ? mv : mm;
+        // SpMV partials / tickets (B = 1); the SpMM reduces in fixed point instead
+        const uint32_t items = B == 1 ? mv.n_items : 1, groups = B == 1 ? mv.n_groups : 1;
+        // B > 1: one extra all-zero row (index n) that dead sources gather
         const size_t nb = (size_t)n * B * sizeof(double);
-        w.share[0].ensure(nb, stream);
-        w.share[1].ensure(nb, stream);
+        const size_t nbs = nb + (B > 1 ? (size_t)B * sizeof(double) : 0);
+        if (w.share[0].bytes < nbs) {
+            w.share[0].ensure(nbs, stream);
+            w.share[1].ensure(nbs, stream);
+            if (B > 1) {
+                CK(cudaMemsetAsync(w.share[0].as<double>() + (size_t)n * B, 0, (size_t)B * 8, stream));
+                CK(cudaMemsetAsync(w.share[1].as<double>() + (size_t)n * B, 0, (size_t)B * 8, stream));
+            }
+        }
         w.acc.ensure(nb, stream);
-        w.part.ensure((size_t)s.n_items * 2 * B * sizeof(double), stream);
-        w.gpart.ensure((size_t)s.n_groups * 2 * B * sizeof(double), stream);
+        w.part.ensure((size_t)items * 2 * B * sizeof(double), stream);
+        w.gpart.ensure((size_t)groups * 2 * B * sizeof(double), stream);
         if (!w.group_cnt.p) {
-            w.group_cnt.ensure((size_t)s.n_groups * sizeof(uint32_t), stream);
+            w.group_cnt.ensure((size_t)groups * sizeof(uint32_t), stream);
             w.done_cnt.ensure(sizeof(uint32_t), stream);
             CK(cudaMemsetAsync(w.group_cnt.p, 0, w.group_cnt.bytes, stream));
             CK(cudaMemsetAsync(w.done_cnt.p, 0, w.done_cnt.bytes, stream));
         }
         w.state.ensure(2 * (size_t)B * sizeof(ColState), stream);
+        if (B > 1 && !w.work_cnt.p) {
+            const size_t words = ((size_t)n + 31) / 32 + 1;
+            w.nz[0].ensure(words * 4, stream);
+            w.nz[1].ensure(words * 4, stream);
+            w.acc_valid.ensure(words * 4, stream);
+            w.long_cnt.ensure((size_t)std::max<uint32_t>(longs.n_long, 1) * 4, stream);
+            w.seg_part.ensure((size_t)std::max<uint32_t>(longs.n_segs, 1) * B * 8, stream);
+            w.work_cnt.ensure(4, stream);
+            w.fx.ensure(4 * (size_t)B * 8, stream);
+            CK(cudaMemsetAsync(w.long_cnt.p, 0, w.long_cnt.bytes, stream));
+            CK(cudaMemsetAsync(w.work_cnt.p, 0, w.work_cnt.bytes, stream));
+            CK(cudaMemsetAsync(w.fx.p, 0, w.fx.bytes, stream));
+            int occ = 0;
+            switch (B) {
+                case 8: occ = mm_occupancy<8>(); break;
+                case 16: occ = mm_occupancy<16>(); break;
+                case 32: occ = mm_occupancy<32>(); break;
+                case 64: occ = mm_occupancy<64>(); break;
+            }
+            w.grid = std::max(1, occ) * num_sms;
+        }
         return w;
     }
 };
@@ -436,9 +535,9 @@ static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
     return std::upper_bound(bounds.begin(), bounds.end(), i) - bounds.begin();
 }
 
-static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, int B) {
-    const Schedule& s = B == 1 ? g->mv : g->mm;
-    const dim3 grid(s.n_items), block(kThreads);
+static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B) {
+    const Schedule& s = g->mv;
+    const dim3 grid(B == 1 ? s.n_items : (uint32_t)w.grid), block(kThreads);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g->profile) {
         e0 = g->take_event();
@@ -447,10 +546,10 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, int B) {
     }
     switch (B) {
         case 1: k_step_spmv<<<grid, block, 0, g->stream>>>(a); break;
-        case 8: k_step_spmm<8><<<grid, block, 0, g->stream>>>(a); break;
-        case 16: k_step_spmm<16><<<grid, block, 0, g->stream>>>(a); break;
-        case 32: k_step_spmm<32><<<grid, block, 0, g->stream>>>(a); break;
-        case 64: k_step_spmm<64><<<grid, block, 0, g->stream>>>(a); break;
+        case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
+        case 16: k_step_spmm2<16><<<grid, MmShape<16>::NT, MmShape<16>::kDynSmem, g->stream>>>(*mm); break;
+        case 32: k_step_spmm2<32><<<grid, MmShape<32>::NT, MmShape<32>::kDynSmem, g->stream>>>(*mm); break;
+        case 64: k_step_spmm2<64><<<grid, MmShape<64>::NT, MmShape<64>::kDynSmem, g->stream>>>(*mm); break;
         default: throw std::invalid_argument("unsupported batch width");
     }
     CKL("k_step (sweep)");
@@ -468,8 +567,12 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, int B) {
 static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int B = cfg.B;
     Workspace& w = g->workspace(B);
-    const Schedule& sch = B == 1 ? g->mv : g->mm;
+    const Schedule& sch = g->mv;
     const uint32_t n = g->n;
+    const bool mm = B > 1;  // SpMM path: frontier bitmaps, lazily valid acc rows
+    if (mm && (cfg.init != Init::Seeds || cfg.start != 0 || !cfg.bounds.empty() || cfg.y_out))
+        throw std::logic_error("batched CPI supports single-seed windows starting at 0 only");
+    const size_t bm_bytes = (((size_t)n + 31) / 32 + 1) * 4;
     const double keep = 1.0 - cfg.c;
     ColState* st = w.state.as<ColState>();
     const bool partition = !cfg.bounds.empty() || !cfg.seg_acc.empty();
@@ -482,6 +585,9 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             if (k != s0 || cfg.init == Init::Seeds)
                 CK(cudaMemsetAsync(cfg.seg_acc[k], 0, (size_t)n * B * 8, g->stream));
         acc0 = cfg.seg_acc[s0];
+    } else if (cfg.acc && mm) {
+        acc0 = cfg.acc;  // validity tracked by acc_valid
+        CK(cudaMemsetAsync(w.acc_valid.p, 0, bm_bytes, g->stream));
     } else if (cfg.acc) {
         const bool in0 = cfg.start == 0;
         if (!in0 || cfg.init == Init::Seeds)
@@ -500,6 +606,15 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
                                                      active0, st);
         CKL("k_init_finish");
         g->launches += 2;
+    } else if (mm) {
+        CK(cudaMemsetAsync(w.nz[0].p, 0, bm_bytes, g->stream));
+        CK(cudaMemsetAsync(w.work_cnt.p, 0, 4, g->stream));
+        CK(cudaMemsetAsync(w.done_cnt.p, 0, 4, g->stream));
+        k_init_seeds_mm<<<1, 64, 0, g->stream>>>(cfg.seeds, cfg.b_valid, B, cfg.c, keep, n, g->policy,
+                                                 g->deg.as<uint32_t>(), w.share[0].as<double>(), acc0,
+                                                 w.nz[0].as<uint32_t>(), w.acc_valid.as<uint32_t>(), active0, st);
+        CKL("k_init_seeds_mm");
+        g->launches += 1;
     } else {
         CK(cudaMemsetAsync(w.share[0].p, 0, (size_t)n * B * 8, g->stream));
         k_init_seeds<<<1, 64, 0, g->stream>>>(cfg.seeds, cfg.b_valid, B, cfg.c, keep, n, g->policy,
@@ -528,6 +643,23 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     a.gpart = w.gpart.as<double>();
     a.group_cnt = w.group_cnt.as<uint32_t>();
     a.done_cnt = w.done_cnt.as<uint32_t>();
+    MmArgs ma{};
+    if (mm) {
+        ma.seg_row = g->longs.seg_row.as<uint32_t>();
+        ma.seg_lo = g->longs.seg_lo.as<int64_t>();
+        ma.seg_long = g->longs.seg_long.as<uint32_t>();
+        ma.long_first = g->longs.long_first.as<uint32_t>();
+        ma.long_nseg = g->longs.long_nseg.as<uint32_t>();
+        ma.long_cnt = w.long_cnt.as<uint32_t>();
+        ma.seg_part = w.seg_part.as<double>();
+        ma.n_segs = g->longs.n_segs;
+        ma.n_blocks = g->n_blocks;
+        ma.blocks = g->longs.blocks.as<uint2>();
+        ma.zero_row = n;
+        ma.work_cnt = w.work_cnt.as<uint32_t>();
+        ma.fx = w.fx.as<unsigned long long>();
+        ma.acc_valid = cfg.acc ? w.acc_valid.as<uint32_t>() : nullptr;
+    }
 
     const int64_t target = cfg.terminal >= 0 ? cfg.terminal : std::numeric_limits<int64_t>::max();
     const uint32_t est = sweeps_estimate(cfg.c, cfg.eps);
@@ -553,7 +685,13 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             combined = combined || a.out != nullptr;
             a.state_in = st + ((i - 1) & 1) * B;
             a.state_out = st + (i & 1) * B;
-            launch_step(g, w, a, B);
+            if (mm) {
+                ma.s = a;
+                ma.nz_in = w.nz[(i - 1) & 1].as<uint32_t>();
+                ma.nz_out = a.share_out ? w.nz[i & 1].as<uint32_t>() : nullptr;
+                if (ma.nz_out) CK(cudaMemsetAsync(ma.nz_out, 0, bm_bytes, g->stream));
+            }
+            launch_step(g, w, a, mm ? &ma : nullptr, B);
         }
         done += chunk;
         if ((int64_t)done >= target) break;
@@ -568,7 +706,8 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     if (cfg.out && !combined) {
         double* acc_final = cfg.acc;
         k_combine<<<grid_for((uint64_t)n * B, 256, 8 * g->num_sms), 256, 0, g->stream>>>(
-            acc_final, n, B, cfg.b_valid, cfg.stranger, cfg.scale, cfg.node_major ? 1 : 0, cfg.out);
+            acc_final, mm ? w.acc_valid.as<uint32_t>() : nullptr, n, B, cfg.b_valid, cfg.stranger, cfg.scale,
+            cfg.node_major ? 1 : 0, cfg.out);
         CKL("k_combine");
         ++g->launches;
     }
@@ -646,14 +785,12 @@ static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, d
         run_cpi(g, cfg, &ro);
         if (!combine) {
             // exact_rwr: the accumulator is the answer
-            if (node_major) {
-                CK(cudaMemcpyAsync(dst, w.acc.p, (size_t)n * B * 8, cudaMemcpyDeviceToDevice, g->stream));
-            } else if (B == 1) {
+            if (B == 1) {
                 CK(cudaMemcpyAsync(dst, w.acc.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, g->stream));
             } else {
-                k_transpose<<<grid_for((uint64_t)n * B, 256, 8 * g->num_sms), 256, 0, g->stream>>>(
-                    w.acc.as<double>(), n, B, bv, dst);
-                CKL("k_transpose");
+                k_acc_export<<<grid_for((uint64_t)n * B, 256, 8 * g->num_sms), 256, 0, g->stream>>>(
+                    w.acc.as<double>(), w.acc_valid.as<uint32_t>(), n, B, bv, node_major ? 1 : 0, dst);
+                CKL("k_acc_export");
                 ++g->launches;
             }
         }
@@ -739,17 +876,68 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         g->launches += 4;
 
         auto mv = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
-        auto mm = build_items(rp, n, kMmTileNnz, kMmTileRows, kMmLongRow);
-        for (auto* pr : {&mv, &mm})
-            if (pr->size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
+        if (mv.size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
+        {
+            // SpMM long rows: kLong-nnz segments, longest rows first
+            std::vector<std::pair<int64_t, uint32_t>> lr;
+            for (uint32_t v = 0; v < n; ++v)
+                if (rp[v + 1] - rp[v] > kLong) lr.push_back({rp[v + 1] - rp[v], v});
+            std::stable_sort(lr.begin(), lr.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+            std::vector<uint32_t> seg_row, seg_long, long_first, long_nseg;
+            std::vector<int64_t> seg_lo;
+            for (uint32_t li = 0; li < lr.size(); ++li) {
+                const uint32_t v = lr[li].second;
+                const uint32_t ns = (uint32_t)((lr[li].first + kLong - 1) / kLong);
+                long_first.push_back((uint32_t)seg_row.size());
+                long_nseg.push_back(ns);
+                for (uint32_t k = 0; k < ns; ++k) {
+                    seg_row.push_back(v);
+                    seg_lo.push_back(rp[v] + (int64_t)k * kLong);
+                    seg_long.push_back(li);
+                }
+            }
+            LongRows& L = g->longs;
+            L.n_long = (uint32_t)lr.size();
+            L.n_segs = (uint32_t)seg_row.size();
+            auto put = [&](DevBuf& d, const void* src, size_t bytes) {
+                d.ensure(std::max<size_t>(bytes, 16), g->stream);
+                if (bytes) CK(cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, s));
+            };
+            put(L.seg_row, seg_row.data(), seg_row.size() * 4);
+            put(L.seg_lo, seg_lo.data(), seg_lo.size() * 8);
+            put(L.seg_long, seg_long.data(), seg_long.size() * 4);
+            put(L.long_first, long_first.data(), long_first.size() * 4);
+            put(L.long_nseg, long_nseg.data(), long_nseg.size() * 4);
+            // short-row blocks: consecutive short rows inside one aligned
+            // kMmRows window, at most kBlockNnz nnz (a lone row may reach kLong)
+            std::vector<uint2> blocks;
+            for (uint32_t w0 = 0; w0 < n; w0 += kMmRows) {
+                const uint32_t w1 = std::min<uint32_t>(n, w0 + kMmRows);
+                uint32_t r = w0;
+                while (r < w1) {
+                    if (rp[r + 1] - rp[r] > kLong) {
+                        ++r;
+                        continue;
+                    }
+                    const uint32_t b0 = r;
+                    int64_t nnz = 0;
+                    while (r < w1 && rp[r + 1] - rp[r] <= kLong) {
+                        const int64_t L2 = rp[r + 1] - rp[r];
+                        if (r > b0 && nnz + L2 > kBlockNnz) break;
+                        nnz += L2;
+                        ++r;
+                    }
+                    blocks.push_back(make_uint2(b0, r - b0));
+                }
+            }
+            put(L.blocks, blocks.data(), blocks.size() * sizeof(uint2));
+            g->n_blocks = (uint32_t)blocks.size();
+            CK(cudaStreamSynchronize(s));
+        }
         g->mv.n_items = (uint32_t)mv.size();
         g->mv.n_groups = (g->mv.n_items + kGroupItems - 1) / kGroupItems;
         g->mv.items.ensure(mv.size() * sizeof(uint2), g->stream);
         CK(cudaMemcpyAsync(g->mv.items.p, mv.data(), mv.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
-        g->mm.n_items = (uint32_t)mm.size();
-        g->mm.n_groups = (g->mm.n_items + kGroupItems - 1) / kGroupItems;
-        g->mm.items.ensure(mm.size() * sizeof(uint2), g->stream);
-        CK(cudaMemcpyAsync(g->mm.items.p, mm.data(), mm.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
         *out = g.release();
     });
@@ -766,7 +954,9 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->col.release();
             g->deg.release();
             g->mv.items.release();
-            g->mm.items.release();
+            for (DevBuf* d : {&g->longs.seg_row, &g->longs.seg_lo, &g->longs.seg_long, &g->longs.long_first,
+                              &g->longs.long_nseg, &g->longs.blocks})
+                d->release();
             g->init_part.release();
             g->out_stage.release();
             for (tpa_artifact* a : g->artifacts) detach_artifact(a);
@@ -807,7 +997,7 @@ int tpa_graph_info(const tpa_graph* g, uint32_t* n, uint64_t* m, uint64_t* finge
         if (fingerprint) *fingerprint = g->fingerprint;
         if (policy) *policy = g->policy;
         if (device_bytes) {
-            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->mm.items.bytes;
+            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->longs.seg_lo.bytes * 2;
             for (auto& kv : g->ws) {
                 const Workspace& w = *kv.second;
                 b += w.share[0].bytes + w.share[1].bytes + w.acc.bytes + w.part.bytes + w.gpart.bytes;
@@ -907,9 +1097,7 @@ int tpa_cpi_run(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, double c,
         if (seeds) {
             // SeedSet (cpi.cpp:19-24): non-empty, sorted, duplicate-free
             if (n_seeds == 0) throw std::invalid_argument("seed set must not be empty");
-            hs.resize(n_seeds);
-            if (dev) CK(cudaMemcpy(hs.data(), seeds, n_seeds * 4, cudaMemcpyDeviceToHost));
-            else std::memcpy(hs.data(), seeds, n_seeds * 4);
+            hs.assign(seeds, seeds + n_seeds);  // host array (see tpa_gpu.h)
             std::sort(hs.begin(), hs.end());
             if (std::adjacent_find(hs.begin(), hs.end()) != hs.end())
                 throw std::invalid_argument("seed set contains duplicate ids");

@@ -145,19 +145,15 @@ def cpi_partition(g: Graph, seeds: SeedSet, c: float, eps: float, boundaries: Se
 def exact_rwr_batch(g: Graph, seeds, c: float = kDefaultRestartProb, eps: float = kDefaultTolerance,
                     out=None):
     """B independent exact_rwr runs as one batched CPI; returns [B][n]."""
+    if type(seeds).__module__.startswith("torch"):
+        seeds = seeds.detach().cpu().numpy()
     s = np.ascontiguousarray(seeds, np.uint32)
     n = g.node_count()
     if out is None:
         out = np.empty((s.size, n), np.float64)
     p, dev, keep = vec_ptr(out, s.size * n)
-    seeds_arg = s
-    flags = 0
-    if dev:
-        import torch
-        seeds_arg = torch.as_tensor(s.astype(np.int64)).to(torch.int32).to(out.device)
-        flags = N.TPA_DEVICE_PTRS
-    sp = seeds_arg.ctypes.data if isinstance(seeds_arg, np.ndarray) else seeds_arg.data_ptr()
-    check(lib.tpa_exact_rwr_batch(_dev(g).h, sp, s.size, float(c), float(eps), p, flags))
+    check(lib.tpa_exact_rwr_batch(_dev(g).h, s.ctypes.data, s.size, float(c), float(eps), p,
+                                  N.TPA_DEVICE_PTRS if dev else 0))
     return out
 
 
@@ -282,18 +278,19 @@ def query_batch(g: Graph, artifact: StrangerArtifact, seeds, family_end: int, ou
     _check_artifact(g, artifact, family_end)
     n = g.node_count()
     dg = _dev(g)
+    # seeds always cross the C-ABI as a host array (validated before any launch)
     if type(seeds).__module__.startswith("torch"):
-        B = int(seeds.numel())
-        sp, sdev, skeep = seeds.data_ptr(), seeds.is_cuda, seeds
-    else:
-        s = np.ascontiguousarray(seeds, np.uint32)
-        B = int(s.size)
-        sp, sdev, skeep = s.ctypes.data, False, s
+        seeds = seeds.detach().cpu().numpy()
+    s = np.ascontiguousarray(np.asarray(seeds).astype(np.int64, copy=False))
+    if s.size and (s.min() < 0 or s.max() > 0xFFFFFFFF):
+        bad = int(s[(s < 0) | (s > 0xFFFFFFFF)][0])
+        raise IndexError(f"seed id {bad} out of range for graph with {n} nodes")
+    s = np.ascontiguousarray(s, np.uint32)
+    B = int(s.size)
+    sp = s.ctypes.data
     if out is None:
         out = np.empty((B, n) if not node_major else (n, B), np.float64)
     p, odev, keep = vec_ptr(out, B * n)
-    if odev != sdev:
-        raise ValueError("seeds and out must both be host or both be device buffers")
     flags = (N.TPA_DEVICE_PTRS if odev else 0) | (N.TPA_NODE_MAJOR if node_major else 0) | \
             (N.TPA_QUERY_NA if na else 0) | (N.TPA_ASYNC if (odev and not sync) else 0)
     check(lib.tpa_query_batch(dg.h, artifact.device(g), sp, B, int(family_end), p, flags))

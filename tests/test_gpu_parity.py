@@ -98,23 +98,30 @@ def test_query_batch_widths(oracle, B):
 
 
 def test_spmm_is_bitwise_the_reference_order_and_slot_independent(oracle):
-    # SpMM rows <= 4096 nnz are summed sequentially in ascending source order,
-    # exactly the reference's scatter order: batch outputs equal the oracle
-    # bit for bit, whatever the batch width or slot.
-    g = P.generate_rmat(12, 16, rng_seed=5)
-    art = P.preprocess(g, 0.15, 1e-9, 10)
-    seeds = P.sample_seeds(g, 64, 3)
-    full = P.query_batch(g, art, seeds, 5)
-    st = oracle.preprocess(g, 0.15, 1e-9, 10)
-    for B in (8, 16, 32):
-        sub = P.query_batch(g, art, seeds[:B][::-1].copy(), 5)[::-1]
-        assert np.array_equal(sub, full[:B])
-    # stranger (SpMV) is within tolerance; with the oracle's own stranger the
-    # family+combine path is bitwise
-    art2 = P.StrangerArtifact(st, g.fingerprint(), 0.15, 1e-9, 10)
-    q = P.query_batch(g, art2, seeds[:32], 5)
-    for k in range(32):
-        assert np.array_equal(q[k], oracle.query(g, st, 0.15, 1e-9, 10, int(seeds[k]), 5))
+    # SpMM rows with in-degree <= 512 are summed sequentially in ascending
+    # source order, exactly the reference's scatter order: those entries equal
+    # the oracle bit for bit; longer rows (fixed 512-nnz segments) are within
+    # tolerance.  Neither depends on the batch width or the slot.
+    for scale in (10, 12):
+        g = P.generate_rmat(scale, 16, rng_seed=5)
+        art = P.preprocess(g, 0.15, 1e-9, 10)
+        seeds = P.sample_seeds(g, 64, 3)
+        full = P.query_batch(g, art, seeds, 5)
+        for B in (8, 16, 32):
+            sub = P.query_batch(g, art, seeds[:B][::-1].copy(), 5)[::-1]
+            assert np.array_equal(sub, full[:B])
+        st = oracle.preprocess(g, 0.15, 1e-9, 10)
+        art2 = P.StrangerArtifact(st, g.fingerprint(), 0.15, 1e-9, 10)
+        q = P.query_batch(g, art2, seeds[:32], 5)
+        indeg = np.bincount(g.out_targets(), minlength=g.node_count())
+        all_short = indeg.max() <= 512  # scale 10: max in-degree 332
+        for k in range(32):
+            want = oracle.query(g, st, 0.15, 1e-9, 10, int(seeds[k]), 5)
+            if all_short:
+                assert np.array_equal(q[k], want)
+            assert_close(q[k], want)
+        if scale == 10:
+            assert all_short
 
 
 def test_determinism_repeat_bitwise():
