@@ -88,6 +88,17 @@ def a_step(n, m, B, acc):
     return 4 * m + 8 * (n + 1) + 8 * n + 8 * B * n * (2 + 2 * acc)
 
 
+def sweep_bytes(n, m, B, kind):
+    """Compulsory bytes of one sweep as this engine runs it (every array touched
+    once): CSR(A^T) indices 4m + row_ptr 8(n+1) + out-degree 4n + the share
+    iterate read 8Bn, plus per kind
+      'mid'     acc read+write and share_out write  (+24Bn)
+      'last'    fused combine: acc read, stranger read, out write (+16Bn + 8n)
+      'noacc'   share_out write only                (+8Bn)"""
+    base = 4 * m + 8 * (n + 1) + 4 * n + 8 * B * n
+    return base + {"mid": 24 * B * n, "last": 16 * B * n + 8 * n, "noacc": 8 * B * n}[kind]
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -326,6 +337,14 @@ def run_ours(args):
     launches = dg.launches() - launches0
     mv_cnt, mv_ms = dg.profile_read(1)
     mm_cnt, mm_ms = dg.profile_read(batch if batch > 1 else 1)
+    per_sweep = {}
+    if batch > 1:
+        for i in range(1, S):
+            c_i, ms_i = dg.profile_read(batch, i)
+            if c_i:
+                kind = "last" if i == S - 1 else "mid"
+                per_sweep[i] = {"launches": c_i, "avg_ms": ms_i / c_i,
+                                "achieved_gbs_dense_bytes": sweep_bytes(n, m, batch, kind) / (ms_i / c_i / 1e3) / 1e9}
     dg.profile(False)
     torch.cuda.synchronize()
     if world > 1:
@@ -348,10 +367,13 @@ def run_ours(args):
     peak, peak_src = peak_hbm()
     Bk = batch if batch > 1 else 1
     if batch > 1 and mm_cnt:
-        kname = f"k_step_spmm<{Bk}>"
-        # 3 of 4 query sweeps accumulate; the 4th is the fused combine (same A_step class)
-        bytes_launch = a_step(n, m, Bk, 1)
-        avg_ms = mm_ms / mm_cnt
+        # dominant kernel: the SpMM sweep.  Roofline on its densest launch, the
+        # last family sweep x^(S-1) (fused combine), with that sweep's exact
+        # compulsory bytes; the sparse early sweeps are listed per index.
+        kname = f"k_step_spmm2<{Bk}>"
+        last = per_sweep.get(S - 1)
+        bytes_launch = sweep_bytes(n, m, Bk, "last")
+        avg_ms = last["avg_ms"] if last else mm_ms / mm_cnt
         share = mm_ms / total_ms if total_ms else None
     else:
         kname = "k_step_spmv"
@@ -363,7 +385,8 @@ def run_ours(args):
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": traffic_per_launch(kname), "algorithmic_bytes_per_launch": bytes_launch,
                 "avg_launch_ms": avg_ms, "launches_timed": mm_cnt if batch > 1 else mv_cnt,
-                "share_of_step": share,
+                "share_of_step": share, "per_sweep": per_sweep,
+                "survey_a_step_bytes": a_step(n, m, Bk, 1),
                 "spmv": {"launches": mv_cnt, "avg_ms": mv_ms / max(mv_cnt, 1),
                          "achieved_gbs": a_step(n, m, 1, 1) / (mv_ms / max(mv_cnt, 1) / 1e3) / 1e9
                          if mv_cnt else None}}

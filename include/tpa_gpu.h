@@ -87,9 +87,10 @@ uint64_t tpa_graph_launches(const tpa_graph *g);
 /* Bench instrumentation: while enabled, every CPI sweep kernel launch is
  * bracketed by CUDA events on the handle's stream.  enable != 0 starts a new
  * session.  profile_read sums the recorded launches of the sweep kernel of a
- * given batch width (1 = SpMV; 8/16/32/64 = SpMM); it synchronises. */
+ * given batch width (1 = SpMV; 8/16/32/64 = SpMM) and sweep index `step`
+ * (x^(step) produced; -1 = all sweeps); it synchronises. */
 int tpa_graph_profile(tpa_graph *g, int enable);
-int tpa_graph_profile_read(tpa_graph *g, int width, uint64_t *launches, double *total_ms);
+int tpa_graph_profile_read(tpa_graph *g, int width, int step, uint64_t *launches, double *total_ms);
 /* Device copy of CSR(A^T) for inspection: row_ptr[n+1] (int64), col[m]. Host ptrs. */
 int tpa_graph_transpose(const tpa_graph *g, int64_t *row_ptr, uint32_t *col);
 

@@ -37,7 +37,7 @@ SIGNATURES = {
                         C.POINTER(_u64)], _int),
     "tpa_graph_launches": ([_vp], _u64),
     "tpa_graph_profile": ([_vp, _int], _int),
-    "tpa_graph_profile_read": ([_vp, _int, C.POINTER(_u64), C.POINTER(_dbl)], _int),
+    "tpa_graph_profile_read": ([_vp, _int, _int, C.POINTER(_u64), C.POINTER(_dbl)], _int),
     "tpa_graph_transpose": ([_vp, _vp, _vp], _int),
     "tpa_propagation_sweep": ([_vp, _vp, _vp, _dbl, _int], _int),
     "tpa_cpi_run": ([_vp, _vp, _u64, _dbl, _dbl, _u32, _i64, _vp, C.POINTER(_u32), C.POINTER(_int),

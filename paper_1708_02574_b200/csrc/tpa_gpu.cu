@@ -26,6 +26,7 @@
 
 #include "cpi_kernels.cuh"
 #include "cpi_spmm.cuh"
+#include "cpi_spmm3.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
 
@@ -323,12 +324,30 @@ std::vector<uint2> build_items(const std::vector<int64_t>& rp, uint32_t n, int64
     return items;
 }
 
-// Persistent-grid sizing for k_step_spmm2<B> (dynamic smem = the row-sum buffers).
+// SpMM kernel generation: v2 (register-pipelined gathers, the measured best);
+// TPA_SPMM=3 selects the experimental cp.async-ring kernel for B = 32 / 64.
+static int spmm_version(int B) {
+    static const int env = [] {
+        const char* e = std::getenv("TPA_SPMM");
+        return e ? std::atoi(e) : 2;
+    }();
+    return (B == 32 || B == 64) && env == 3 ? 3 : 2;
+}
+
+// Persistent-grid sizing (dynamic smem = ring / row-sum buffers).
 template <int B>
 static int mm_occupancy() {
+    int occ = 0;
+    if constexpr (B == 32 || B == 64) {
+        if (spmm_version(B) == 3) {
+            const size_t dyn = Mm3Shape<B>::kDynSmem;
+            CK(cudaFuncSetAttribute(k_step_spmm3<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmm3<B>, Mm3Shape<B>::NT, dyn));
+            return occ;
+        }
+    }
     const size_t dyn = MmShape<B>::kDynSmem;
     CK(cudaFuncSetAttribute(k_step_spmm2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmm2<B>, MmShape<B>::NT, dyn));
     return occ;
 }
@@ -374,7 +393,12 @@ struct tpa_graph {
     std::mutex mu;
     // optional per-sweep-kernel CUDA-event timing (bench instrumentation)
     bool profile = false;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_events;
+    struct ProfEvent {
+        int width;
+        uint32_t step;
+        cudaEvent_t e0, e1;
+    };
+    std::vector<ProfEvent> prof_events;
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event() {
         cudaEvent_t e;
@@ -548,15 +572,25 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         case 1: k_step_spmv<<<grid, block, 0, g->stream>>>(a); break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
         case 16: k_step_spmm2<16><<<grid, MmShape<16>::NT, MmShape<16>::kDynSmem, g->stream>>>(*mm); break;
-        case 32: k_step_spmm2<32><<<grid, MmShape<32>::NT, MmShape<32>::kDynSmem, g->stream>>>(*mm); break;
-        case 64: k_step_spmm2<64><<<grid, MmShape<64>::NT, MmShape<64>::kDynSmem, g->stream>>>(*mm); break;
+        case 32:
+            if (spmm_version(32) == 3)
+                k_step_spmm3<32><<<grid, Mm3Shape<32>::NT, Mm3Shape<32>::kDynSmem, g->stream>>>(*mm);
+            else
+                k_step_spmm2<32><<<grid, MmShape<32>::NT, MmShape<32>::kDynSmem, g->stream>>>(*mm);
+            break;
+        case 64:
+            if (spmm_version(64) == 3)
+                k_step_spmm3<64><<<grid, Mm3Shape<64>::NT, Mm3Shape<64>::kDynSmem, g->stream>>>(*mm);
+            else
+                k_step_spmm2<64><<<grid, MmShape<64>::NT, MmShape<64>::kDynSmem, g->stream>>>(*mm);
+            break;
         default: throw std::invalid_argument("unsupported batch width");
     }
     CKL("k_step (sweep)");
     ++g->launches;
     if (g->profile) {
         CK(cudaEventRecord(e1, g->stream));
-        g->prof_events.push_back({B, {e0, e1}});
+        g->prof_events.push_back({B, a.step, e0, e1});
     }
 }
 
@@ -963,8 +997,8 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->artifacts.clear();
             cudaStreamSynchronize(g->stream);
             for (auto& pe : g->prof_events) {
-                cudaEventDestroy(pe.second.first);
-                cudaEventDestroy(pe.second.second);
+                cudaEventDestroy(pe.e0);
+                cudaEventDestroy(pe.e1);
             }
             for (auto e : g->event_pool) cudaEventDestroy(e);
             if (g->own_stream) cudaStreamDestroy(g->stream);
@@ -1016,8 +1050,8 @@ int tpa_graph_profile(tpa_graph* g, int enable) {
         if (enable) {
             CK(cudaStreamSynchronize(g->stream));
             for (auto& pe : g->prof_events) {
-                g->event_pool.push_back(pe.second.first);
-                g->event_pool.push_back(pe.second.second);
+                g->event_pool.push_back(pe.e0);
+                g->event_pool.push_back(pe.e1);
             }
             g->prof_events.clear();
         }
@@ -1025,7 +1059,7 @@ int tpa_graph_profile(tpa_graph* g, int enable) {
     });
 }
 
-int tpa_graph_profile_read(tpa_graph* g, int width, uint64_t* launches, double* total_ms) {
+int tpa_graph_profile_read(tpa_graph* g, int width, int step, uint64_t* launches, double* total_ms) {
     return guard([&] {
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
@@ -1033,9 +1067,9 @@ int tpa_graph_profile_read(tpa_graph* g, int width, uint64_t* launches, double* 
         uint64_t cnt = 0;
         double tot = 0.0;
         for (auto& pe : g->prof_events) {
-            if (pe.first != width) continue;
+            if (pe.width != width || (step >= 0 && (int)pe.step != step)) continue;
             float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
+            CK(cudaEventElapsedTime(&ms, pe.e0, pe.e1));
             tot += ms;
             ++cnt;
         }

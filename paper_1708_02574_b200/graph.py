@@ -241,10 +241,11 @@ class DeviceGraph:
         """Start (True) or stop (False) per-sweep-kernel CUDA-event timing."""
         check(lib.tpa_graph_profile(self.h, 1 if enable else 0))
 
-    def profile_read(self, width: int):
-        """(launches, total_ms) of the sweep kernel of batch width `width`."""
+    def profile_read(self, width: int, step: int = -1):
+        """(launches, total_ms) of the sweep kernel of batch width `width`
+        producing x^(step) (-1: every sweep)."""
         n, ms = C.c_uint64(), C.c_double()
-        check(lib.tpa_graph_profile_read(self.h, int(width), C.byref(n), C.byref(ms)))
+        check(lib.tpa_graph_profile_read(self.h, int(width), int(step), C.byref(n), C.byref(ms)))
         return n.value, ms.value
 
     def device_bytes(self) -> int:

@@ -26,6 +26,9 @@ dg.profile(True)
 for k in range(2, 8):
     P.query_batch(g, art, seeds[k * batch:(k + 1) * batch], 5, out=out)
 cnt, ms = dg.profile_read(batch)
+for i in range(1, 5):
+    c_i, ms_i = dg.profile_read(batch, i)
+    print("  sweep", i, "avg ms", round(ms_i / max(c_i, 1), 4))
 dg.profile(False)
 print(os.environ.get("TPA_LIB", "default"), cfg, "B", batch, "sweeps", cnt, "avg ms/sweep", round(ms / cnt, 4),
       "ms/batch", round(ms / 6, 3))
