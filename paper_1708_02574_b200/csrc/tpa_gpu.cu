@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <limits>
 #include <map>
 #include <memory>
@@ -36,6 +37,12 @@ std::string& last_error() {
     thread_local std::string s;
     return s;
 }
+
+// Set by an atexit hook registered at the first graph creation (so it runs
+// before the static CUDA runtime tears down): handles destroyed after that
+// point (static destructors of a host program) are leaked instead of freed.
+std::atomic<bool> g_exiting{false};
+void mark_exiting() { g_exiting = true; }
 
 #define CK(x)                                                                            \
     do {                                                                                 \
@@ -852,6 +859,8 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         if (policy < 0 || policy > 2) throw std::invalid_argument("unknown dangling policy");
         if (out_offsets[n] != m) throw std::invalid_argument("out_offsets[n] != m");
         DeviceGuard dg(device);
+        static std::once_flag once;
+        std::call_once(once, [] { std::atexit(mark_exiting); });
         {
             const cudaError_t stale = cudaGetLastError();
             if (stale != cudaSuccess && std::getenv("TPA_DEBUG"))
@@ -980,6 +989,7 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
 int tpa_graph_destroy(tpa_graph* g) {
     return guard([&] {
         if (!g) return;
+        if (g_exiting) return;  // process exit: the CUDA runtime may already be gone
         {
             DeviceGuard dg(g->device);
             // stream-ordered frees first, then drain and drop the stream
@@ -1314,6 +1324,7 @@ int tpa_artifact_create(tpa_graph* g, const double* stranger, uint64_t graph_fin
 int tpa_artifact_destroy(tpa_artifact* a) {
     return guard([&] {
         if (!a) return;
+        if (g_exiting) return;
         if (tpa_graph* g = a->g) {
             std::lock_guard<std::mutex> lk(g->mu);
             DeviceGuard dg(g->device);
