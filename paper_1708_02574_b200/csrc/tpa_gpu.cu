@@ -28,6 +28,7 @@
 #include "cpi_kernels.cuh"
 #include "cpi_spmm.cuh"
 #include "cpi_spmm3.cuh"
+#include "cpi_spmm4.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
 
@@ -331,14 +332,31 @@ std::vector<uint2> build_items(const std::vector<int64_t>& rp, uint32_t n, int64
     return items;
 }
 
-// SpMM kernel generation: v2 (register-pipelined gathers, the measured best);
-// TPA_SPMM=3 selects the experimental cp.async-ring kernel for B = 32 / 64.
+// SpMM kernel generation for B = 32 / 64: v4 (lean gather + coalesced
+// epilogue, the measured best) unless TPA_SPMM selects 2 (fused, register
+// pipelined) or 3 (experimental cp.async ring).  B = 8 / 16 always use v2.
 static int spmm_version(int B) {
     static const int env = [] {
         const char* e = std::getenv("TPA_SPMM");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 4;
     }();
-    return (B == 32 || B == 64) && env == 3 ? 3 : 2;
+    if (B != 32 && B != 64) return 2;
+    return env == 2 || env == 3 ? env : 4;
+}
+
+template <int B>
+constexpr size_t mm4_epi_smem() {
+    return (size_t)(Mm4<B>::NT / 32) * 32 * (B + 1) * sizeof(double);
+}
+
+template <int B>
+static void mm4_grids(int num_sms, int& g_gather, int& g_epi) {
+    int o1 = 0, o2 = 0;
+    CK(cudaFuncSetAttribute(k_mm_epi<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm4_epi_smem<B>()));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_mm_gather<B>, Mm4<B>::NT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_mm_epi<B>, Mm4<B>::NT, mm4_epi_smem<B>()));
+    g_gather = std::max(1, o1) * num_sms;
+    g_epi = std::max(1, o2) * num_sms;
 }
 
 // Persistent-grid sizing (dynamic smem = ring / row-sum buffers).
@@ -365,6 +383,8 @@ struct Workspace {
     // SpMM (B > 1) extras
     DevBuf nz[2], acc_valid, long_cnt, seg_part, work_cnt, fx;
     int grid = 0;  // persistent grid of k_step_spmm2<B>
+    DevBuf Y, ybits;  // v4: row sums and their written-rows bitmap
+    int grid_gather = 0, grid_epi = 0;
 };
 
 // Long rows of CSR(Ãᵀ) (in-degree > kLong) cut into kLong-nnz segments, the
@@ -468,6 +488,12 @@ struct tpa_graph {
                 case 64: occ = mm_occupancy<64>(); break;
             }
             w.grid = std::max(1, occ) * num_sms;
+            if (spmm_version(B) == 4) {
+                w.Y.ensure((size_t)n * B * 8, stream);
+                w.ybits.ensure(words * 4, stream);
+                if (B == 32) mm4_grids<32>(num_sms, w.grid_gather, w.grid_epi);
+                if (B == 64) mm4_grids<64>(num_sms, w.grid_gather, w.grid_epi);
+            }
         }
         return w;
     }
@@ -575,7 +601,21 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         e1 = g->take_event();
         CK(cudaEventRecord(e0, g->stream));
     }
-    switch (B) {
+    const bool v4 = B > 1 && spmm_version(B) == 4;
+    if (v4) {
+        Mm4Args P{*mm, w.Y.as<double>(), w.ybits.as<uint32_t>()};
+        CK(cudaMemsetAsync(w.ybits.p, 0, w.ybits.bytes, g->stream));
+        if (B == 32) {
+            k_mm_gather<32><<<w.grid_gather, Mm4<32>::NT, 0, g->stream>>>(P);
+            CKL("k_mm_gather<32>");
+            k_mm_epi<32><<<w.grid_epi, Mm4<32>::NT, mm4_epi_smem<32>(), g->stream>>>(P);
+        } else {
+            k_mm_gather<64><<<w.grid_gather, Mm4<64>::NT, 0, g->stream>>>(P);
+            CKL("k_mm_gather<64>");
+            k_mm_epi<64><<<w.grid_epi, Mm4<64>::NT, mm4_epi_smem<64>(), g->stream>>>(P);
+        }
+        g->launches += 1;
+    } else switch (B) {
         case 1: k_step_spmv<<<grid, block, 0, g->stream>>>(a); break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
         case 16: k_step_spmm2<16><<<grid, MmShape<16>::NT, MmShape<16>::kDynSmem, g->stream>>>(*mm); break;

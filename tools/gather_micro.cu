@@ -1,0 +1,150 @@
+// gather_micro.cu -- microbenchmark: random 256-B row gathers (the SpMM's
+// access pattern at B = 32 fp64) through three paths, to find which one can
+// keep the most requests in flight per SM on the B200.
+//   A: LDG into registers (lane = column), U rows in flight per warp
+//   B: cp.async.bulk (bulk-copy / TMA engine) of whole rows into a per-warp
+//      shared-memory ring, one row per lane per instruction, mbarrier-tracked
+//   C: cp.async (LDGSTS) 16 B per lane into the same ring
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_micro tools/gather_micro.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <vector>
+#include <random>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
+
+constexpr int B = 32;  // doubles per row (256 B)
+
+template <int U>
+__global__ void gather_ldg(const double* __restrict__ X, const uint32_t* __restrict__ idx, long long m, double* out) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = (m + nw - 1) / nw;
+    const long long lo = warp * per, hi = min(m, lo + per);
+    double s = 0.0;
+    for (long long e = lo; e < hi; e += U) {
+        double v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t u = e + j < hi ? __ldg(idx + e + j) : 0u;
+            v[j] = __ldg(X + (size_t)u * B + lane);
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) s += v[j];
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n LAB_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LAB_WAIT;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(phase));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                     "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                 "r"((uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+
+// B: each warp owns a ring of S stages x 32 rows; stage k's 32 rows are issued
+// by the 32 lanes (one bulk copy each), completion on mbar[k].
+template <int S>
+__global__ void gather_bulk(const double* __restrict__ X, const uint32_t* __restrict__ idx, long long m, double* out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem) + (size_t)w * S * 32 * B;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nwb * S * 32 * B * 8) + w * S;
+    if (lane < S) mbar_init(&bars[lane], 1);
+    __syncwarp();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = ((m + nw - 1) / nw + 31) / 32 * 32;
+    const long long lo = warp * per, hi = min(m, lo + per);
+    const long long nst = (hi > lo) ? (hi - lo + 31) / 32 : 0;
+    auto issue = [&](long long k) {
+        if (k >= nst) return;
+        const int slot = (int)(k % S);
+        const long long e = lo + k * 32 + lane;
+        const int cnt = (int)min(32LL, hi - (lo + k * 32));
+        if (lane == 0) mbar_expect_tx(&bars[slot], cnt * B * 8);
+        __syncwarp();
+        if (lane < cnt) bulk_g2s(ring + ((size_t)slot * 32 + lane) * B, X + (size_t)__ldg(idx + e) * B, B * 8, &bars[slot]);
+    };
+    for (int k = 0; k < S; ++k) issue(k);
+    double s = 0.0;
+    for (long long k = 0; k < nst; ++k) {
+        const int slot = (int)(k % S);
+        mbar_wait(&bars[slot], (uint32_t)((k / S) & 1));
+        const int cnt = (int)min(32LL, hi - (lo + k * 32));
+        for (int j = 0; j < cnt; ++j) s += ring[((size_t)slot * 32 + j) * B + lane];
+        __syncwarp();
+        issue(k + S);
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
+int main(int argc, char** argv) {
+    const uint32_t n = 1 << 20;
+    const long long m = 16586831;
+    double* X;
+    uint32_t* idx;
+    double* out;
+    CK(cudaMalloc(&X, (size_t)n * B * 8));
+    CK(cudaMalloc(&idx, m * 4));
+    CK(cudaMalloc(&out, 8));
+    CK(cudaMemset(X, 0, (size_t)n * B * 8));
+    std::vector<uint32_t> h(m);
+    std::mt19937_64 rng(1);
+    // skewed like R-MAT: mix of hub-heavy and uniform sources
+    for (long long i = 0; i < m; ++i) {
+        const double r = (rng() >> 11) * 0x1p-53;
+        h[i] = r < 0.5 ? (uint32_t)(rng() % 16384) : (uint32_t)(rng() % n);
+    }
+    CK(cudaMemcpy(idx, h.data(), m * 4, cudaMemcpyHostToDevice));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto timeit = [&](const char* name, auto launch) {
+        launch();
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(e0);
+        for (int r = 0; r < 5; ++r) launch();
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 5;
+        printf("%-34s %8.3f ms  %6.1f G gathers/s  %7.0f GB/s\n", name, ms, m / ms / 1e6, m * 256.0 / ms / 1e6);
+    };
+    for (int warps : {16, 32, 48, 64}) {
+        char nm[64];
+        snprintf(nm, 64, "LDG U=16, %d warps/SM", warps);
+        timeit(nm, [&] { gather_ldg<16><<<sms * warps / 8, 256>>>(X, idx, m, out); });
+    }
+    for (int S : {2, 4}) {
+        for (int wpb : {4, 8}) {
+            const size_t smem = (size_t)wpb * S * 32 * B * 8 + wpb * S * 8;
+            auto k = S == 2 ? gather_bulk<2> : gather_bulk<4>;
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, wpb * 32, smem);
+            char nm[80];
+            snprintf(nm, 80, "bulk S=%d, %d warps/CTA x %d CTA/SM", S, wpb, occ);
+            timeit(nm, [&] { k<<<sms * occ, wpb * 32, smem>>>(X, idx, m, out); });
+        }
+    }
+    return 0;
+}
