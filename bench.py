@@ -370,13 +370,14 @@ def run_ours(args):
         # dominant kernel: the SpMM sweep.  Roofline on its densest launch, the
         # last family sweep x^(S-1) (fused combine), with that sweep's exact
         # compulsory bytes; the sparse early sweeps are listed per index.
-        kname = f"k_step_spmm2<{Bk}>"
+        kname = (f"k_mm_gather<{Bk}> + k_mm_epi<{Bk}>" if Bk in (32, 64) and os.environ.get("TPA_SPMM", "4") == "4"
+                 else f"k_step_spmm2<{Bk}>")
         last = per_sweep.get(S - 1)
         bytes_launch = sweep_bytes(n, m, Bk, "last")
         avg_ms = last["avg_ms"] if last else mm_ms / mm_cnt
         share = mm_ms / total_ms if total_ms else None
     else:
-        kname = "k_step_spmv"
+        kname = "k_step_spmv2" if os.environ.get("TPA_SPMV", "2") == "2" else "k_step_spmv"
         bytes_launch = a_step(n, m, 1, 1)
         avg_ms = mv_ms / max(mv_cnt, 1)
         share = mv_ms / total_ms if total_ms else None

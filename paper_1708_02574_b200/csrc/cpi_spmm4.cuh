@@ -37,7 +37,59 @@ struct Mm4Args {
     MmArgs m;               // graph, state, bitmaps, segments, reduction (reused)
     double* __restrict__ Y; // [n][B] row sums
     uint32_t* __restrict__ ybits;  // rows of Y written (nonzero), pre-zeroed
+    const uint8_t* __restrict__ rowflag;   // rows that can be nonzero (sparse sweeps), or null
+    const int* dense;                      // set by k_mark_out when the frontier is too big
+    const uint2* __restrict__ blocks_rb;   // v5: blocks of <= Mm5<B>::RB rows
+    uint32_t n_blocks_rb;
 };
+
+// Direction-optimised sparse sweeps.  A frontier row is a row of share_in
+// that is not all-zero (nz bitmap).  k_frontier_cost sums the frontier's
+// out-degrees; if the push would touch at most `limit` edges, k_mark_out sets
+// rowflag[v] = 1 for every out-neighbour v of the frontier (plain byte stores:
+// idempotent, no atomics), otherwise it flags the sweep dense.  A row left
+// unmarked has no live in-neighbour, so its pull sum is exactly zero and the
+// gather kernel skips it.  One warp per 32-row frontier word.
+__global__ void __launch_bounds__(256) k_frontier_cost(const uint32_t* __restrict__ nz, uint32_t n_words,
+                                                       const uint64_t* __restrict__ out_off,
+                                                       unsigned long long* cost) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long c = 0;
+    for (uint32_t w = gw; w < n_words; w += nw) {
+        const uint32_t bits = __ldg(nz + w);
+        if ((bits >> lane) & 1u) {
+            const uint32_t u = w * 32 + lane;
+            c += __ldg(out_off + u + 1) - __ldg(out_off + u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0 && c) atomicAdd(cost, c);
+}
+
+__global__ void __launch_bounds__(256) k_mark_out(const uint32_t* __restrict__ nz, uint32_t n_words,
+                                                  const uint64_t* __restrict__ out_off,
+                                                  const uint32_t* __restrict__ out_tgt,
+                                                  const unsigned long long* cost, unsigned long long limit,
+                                                  uint8_t* rowflag, int* dense) {
+    if (*cost > limit) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *dense = 1;
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = gw; w < n_words; w += nw) {
+        uint32_t bits = __ldg(nz + w);
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const uint32_t u = w * 32 + b;
+            const uint64_t lo = __ldg(out_off + u), hi = __ldg(out_off + u + 1);
+            for (uint64_t e = lo + lane; e < hi; e += 32) rowflag[__ldg(out_tgt + e)] = 1;
+        }
+    }
+}
 
 template <int B>
 __global__ void __launch_bounds__(Mm4<B>::NT, 5) k_mm_gather(Mm4Args P) {
@@ -51,6 +103,7 @@ __global__ void __launch_bounds__(Mm4<B>::NT, 5) k_mm_gather(Mm4Args P) {
     const double* __restrict__ share = a.share_in;
     const uint32_t total = A.n_segs + A.n_blocks;
 
+    const bool use_mask = P.rowflag != nullptr && *P.dense == 0;
     uint32_t next_item = 0;
     if (lane == 0) next_item = atomicAdd(A.work_cnt, 1u);
     for (;;) {
@@ -61,6 +114,15 @@ __global__ void __launch_bounds__(Mm4<B>::NT, 5) k_mm_gather(Mm4Args P) {
         uint32_t r0;
         int nrows;
         int64_t rpl;  // lane k: row_ptr[r0 + k] (k <= nrows)
+        if (use_mask) {
+            // sparse sweep: skip items whose rows cannot receive anything
+            // (a long row is marked or not as a whole, so either all of its
+            // segments run -- and the last one finishes it -- or none does)
+            const uint32_t rr = is_seg ? A.seg_row[item] : A.blocks[item - A.n_segs].x;
+            const uint32_t nrr = is_seg ? 1u : A.blocks[item - A.n_segs].y;
+            const bool mk = lane < (int)nrr && P.rowflag[rr + lane];
+            if (!__any_sync(0xffffffffu, mk)) continue;
+        }
         if (is_seg) {
             r0 = A.seg_row[item];
             nrows = 1;

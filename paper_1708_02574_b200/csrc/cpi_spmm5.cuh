@@ -1,0 +1,358 @@
+// cpi_spmm5.cuh -- K3 v5: the B-seed sweep (B = 32, 64) as ONE lean kernel.
+//
+// v4's gather stream (lane = column, 16 gathers in flight, strictly
+// sequential per-row sums) with the epilogue folded back in, without the
+// per-warp register weight that capped v2 at 16 warps/SM:
+//   * at block start the block's accumulator rows are copied global -> shared
+//     by cp.async (they arrive while the gathers run: no exposed round trip);
+//   * a closing row only stores its B sums to a small shared buffer;
+//   * after the stream the warp walks the block's <= 16 rows in a rolled
+//     loop: acc += y, share_out = keep*y/deg (mid sweeps) or the combine
+//     out = (1+nsf)*acc + stranger staged in the same shared tile and written
+//     transposed (256-byte contiguous stores into the seed-major output);
+//   * bitmaps and the fixed-point residual as in v2/v4.
+// No Y round trip through HBM, one launch per sweep.
+#pragma once
+
+#include "cpi_spmm4.cuh"
+
+namespace tpa {
+
+template <int B>
+struct Mm5 {
+    static_assert(B == 32 || B == 64, "v5: one warp per row group");
+    static constexpr int CPL = B / 32;
+    static constexpr int U = 16 / CPL;         // gathers in flight per lane
+    static constexpr int RB = B == 32 ? 16 : 8;  // rows per block (smem per warp ~8 KiB)
+    static constexpr int NW = 4;               // warps per CTA
+    static constexpr int NT = NW * 32;
+    static constexpr int TS = B + 2;           // padded row stride (doubles) of the tile
+    static constexpr size_t kYBytes = (size_t)RB * B * 8;
+    static constexpr size_t kTBytes = (size_t)RB * TS * 8;
+    static constexpr size_t kWarpBytes = kYBytes + kTBytes;
+    static constexpr size_t kDynSmem = NW * kWarpBytes;
+};
+
+template <int CPL>
+__device__ __forceinline__ void cp_async_acc(double* dst_smem, const double* src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+    if constexpr (CPL == 1)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int B, bool kLast>
+__global__ void __launch_bounds__(Mm5<B>::NT, 8) k_mm_fused(Mm4Args P) {
+    using Sh = Mm5<B>;
+    constexpr int CPL = Sh::CPL, U = Sh::U, TS = Sh::TS;
+    const MmArgs& A = P.m;
+    const StepArgs& a = A.s;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    __shared__ ColState s_st[B];
+    __shared__ unsigned long long s_fx[4 * B];
+    __shared__ uint32_t s_ticket;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c0 = lane * CPL;
+    double (*yb)[B] = reinterpret_cast<double (*)[B]>(s_dyn + (size_t)wid * Sh::kWarpBytes);
+    double* tile = reinterpret_cast<double*>(s_dyn + (size_t)wid * Sh::kWarpBytes + Sh::kYBytes);
+
+    for (int i = tid; i < 4 * B; i += Sh::NT) s_fx[i] = 0ull;
+    for (int b = tid; b < B; b += Sh::NT) s_st[b] = a.state_in[b];
+    __syncthreads();
+    ColState st[CPL];
+    bool any_active = false;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        st[c] = s_st[c0 + c];
+        any_active = any_active || st[c].active;
+    }
+    any_active = __any_sync(0xffffffffu, any_active);
+    const bool want_dm = a.policy == kUniform;
+    unsigned long long fx[4][CPL];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) fx[q][c] = 0ull;
+
+    const uint32_t* __restrict__ col = a.col;
+    const uint32_t* __restrict__ nz = A.nz_in;
+    const double* __restrict__ share = a.share_in;
+    const uint32_t total = A.n_segs + P.n_blocks_rb;
+    const bool use_mask = P.rowflag != nullptr && *P.dense == 0;
+    const bool work = any_active || kLast;
+
+    uint32_t next_item = 0;
+    if (work && lane == 0) next_item = atomicAdd(A.work_cnt, 1u);
+    while (work) {
+        const uint32_t item = __shfl_sync(0xffffffffu, next_item, 0);
+        if (item >= total) break;
+        if (lane == 0) next_item = atomicAdd(A.work_cnt, 1u);
+        const bool is_seg = item < A.n_segs;
+        uint32_t r0;
+        int nrows;
+        if (is_seg) {
+            r0 = A.seg_row[item];
+            nrows = 1;
+        } else {
+            const uint2 blk = P.blocks_rb[item - A.n_segs];
+            r0 = blk.x;
+            nrows = (int)blk.y;
+        }
+        // sparse sweep: skip items none of whose rows the frontier reaches
+        // (unless a combine still has to produce them)
+        if (use_mask && !kLast) {
+            const bool mk = lane < nrows && P.rowflag[r0 + lane];
+            if (!__any_sync(0xffffffffu, mk)) continue;
+        }
+        int64_t rpl;
+        if (is_seg) {
+            const int64_t lo = A.seg_lo[item];
+            const int64_t hi = min(lo + (int64_t)kLong, (int64_t)__ldg(a.row_ptr + r0 + 1));
+            rpl = lane == 0 ? lo : hi;
+        } else {
+            rpl = lane <= nrows ? __ldg(a.row_ptr + r0 + lane) : 0;
+        }
+        // block epilogue inputs, fetched now so they land during the gathers
+        const uint32_t av = (A.acc_valid && a.acc) ? __ldcg(A.acc_valid + (r0 >> 5)) : 0u;
+        const uint32_t dl = lane < nrows ? __ldg(a.deg + r0 + lane) : 0u;
+        if (!is_seg && a.acc) {
+            for (int k = 0; k < nrows; ++k)
+                if ((av >> ((r0 + k) & 31)) & 1u)
+                    cp_async_acc<CPL>(tile + k * TS + c0, a.acc + (size_t)(r0 + k) * B + c0);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+
+        const int64_t e0 = __shfl_sync(0xffffffffu, rpl, 0);
+        const int64_t e1 = __shfl_sync(0xffffffffu, rpl, nrows);
+        const int64_t rpn = __shfl_down_sync(0xffffffffu, rpl, 1);
+        const bool starts = !is_seg && lane >= 1 && lane < nrows && rpn > rpl && rpl > e0;
+        const uint32_t ne_mask = __ballot_sync(0xffffffffu, lane < nrows && rpn > rpl);
+        int cur = ne_mask ? __ffs(ne_mask) - 1 : 0;
+        double s[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) s[c] = 0.0;
+        for (int k = 0; k < nrows; ++k)
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) yb[k][c0 + c] = 0.0;
+        auto close_row = [&](int k_next) {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                yb[cur][c0 + c] = s[c];
+                s[c] = 0.0;
+            }
+            cur = k_next;
+        };
+        auto idx_at = [&](int64_t base) -> uint32_t {
+            const int64_t e = base + lane;
+            return (lane < U && e < e1) ? ld_stream_u32(col + e) : 0u;
+        };
+        auto bits_at = [&](uint32_t u, int64_t base) -> uint32_t {
+            return (nz && lane < U && base + lane < e1) ? __ldg(nz + (u >> 5)) : 0xffffffffu;
+        };
+        if (any_active && e1 > e0) {
+            uint32_t i0 = idx_at(e0), i1 = idx_at(e0 + U);
+            uint32_t w0 = bits_at(i0, e0);
+            for (int64_t base = e0; base < e1; base += U) {
+                const uint32_t i2 = idx_at(base + 2 * U);
+                const uint32_t w1 = bits_at(i1, base + U);
+                const bool live = (w0 >> (i0 & 31)) & 1u;
+                const uint32_t lmask = __ballot_sync(0xffffffffu, live && lane < U && base + lane < e1);
+                const int64_t p = rpl - base;
+                const uint32_t smask = __ballot_sync(0xffffffffu, starts && p >= 0 && p < U);
+                if (lmask) {
+                    double v[U][CPL];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t u = __shfl_sync(0xffffffffu, i0, j);
+                        if ((lmask >> j) & 1u) {
+                            ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
+                        }
+                    }
+                    if (smask == 0) {
+#pragma unroll
+                        for (int j = 0; j < U; ++j)
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                    } else {
+                        uint32_t m = smask;
+                        int pos_next = U, k_next = 0;
+                        if (m) {
+                            k_next = __ffs(m) - 1;
+                            m &= m - 1;
+                            pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
+                        }
+#pragma unroll
+                        for (int j = 0; j < U; ++j) {
+                            if (j == pos_next) {  // warp-uniform
+                                close_row(k_next);
+                                if (m) {
+                                    k_next = __ffs(m) - 1;
+                                    m &= m - 1;
+                                    pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
+                                } else {
+                                    pos_next = U;
+                                }
+                            }
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                        }
+                    }
+                } else if (smask) {
+                    uint32_t m = smask;
+                    while (m) {
+                        const int k = __ffs(m) - 1;
+                        m &= m - 1;
+                        close_row(k);
+                    }
+                }
+                i0 = i1;
+                i1 = i2;
+                w0 = w1;
+            }
+        }
+        if (is_seg) {
+            // publish the segment; the last one of the row combines in order
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) A.seg_part[(size_t)item * B + c0 + c] = s[c];
+            __threadfence();
+            __syncwarp();
+            const uint32_t li = A.seg_long[item];
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(A.long_cnt + li, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t != A.long_nseg[li] - 1) continue;
+            __threadfence();
+            const uint32_t f0 = A.long_first[li], ns = A.long_nseg[li];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                double y = __ldcg(A.seg_part + (size_t)f0 * B + c0 + c);
+                for (uint32_t j = 1; j < ns; ++j) y = dadd(y, __ldcg(A.seg_part + (size_t)(f0 + j) * B + c0 + c));
+                yb[0][c0 + c] = y;
+            }
+            if (lane == 0) A.long_cnt[li] = 0;
+            if (a.acc && ((av >> (r0 & 31)) & 1u)) cp_async_acc<CPL>(tile + c0, a.acc + (size_t)r0 * B + c0);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        } else if (ne_mask) {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) yb[cur][c0 + c] = s[c];
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+
+        // ---- block epilogue: rows r0 .. r0+nrows-1 ----
+        double bl1[CPL], bdm[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) bl1[c] = bdm[c] = 0.0;
+        uint32_t nzw = 0, avw = 0;
+        for (int k = 0; k < nrows; ++k) {
+            const uint32_t r = r0 + k;
+            const bool valid = (av >> (r & 31)) & 1u;
+            double yy[CPL], ao[CPL];
+            bool nzc = false;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                yy[c] = yb[k][c0 + c];
+                if (st[c].has_spread) yy[c] = dadd(yy[c], st[c].spread);  // graph.cpp:265-268
+                if (!st[c].active) yy[c] = 0.0;
+                ao[c] = valid ? tile[k * TS + c0 + c] : 0.0;
+                nzc = nzc || yy[c] != 0.0;
+            }
+            const bool row_nz = __any_sync(0xffffffffu, nzc);
+            if (!kLast && !row_nz) continue;  // nothing changes for this row
+            const uint32_t d = __shfl_sync(0xffffffffu, dl, k);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const size_t ix = (size_t)r * B + c0 + c;
+                if (!st[c].active) {
+                    if (kLast) tile[k * TS + c0 + c] = combine_value(a, ao[c], r);
+                    else if (!valid) a.acc[ix] = 0.0;  // the row becomes valid below
+                    continue;
+                }
+                const double f = dadd(ao[c], yy[c]);  // cpi.cpp:50
+                if (kLast) {
+                    tile[k * TS + c0 + c] = combine_value(a, f, r);  // tpa.cpp:73-74
+                } else {
+                    a.acc[ix] = f;
+                    a.share_out[ix] = d ? ddiv(dmul(a.keep, yy[c]), (double)d) : 0.0;  // graph.cpp:222
+                }
+                bl1[c] = dadd(bl1[c], fabs(yy[c]));
+                if (want_dm && d == 0) bdm[c] = dadd(bdm[c], yy[c]);
+            }
+            nzw |= (row_nz ? 1u : 0u) << (r & 31);
+            avw |= 1u << (r & 31);
+        }
+        if (kLast) {
+            __syncwarp();
+            if (a.out_node_major) {
+                for (int k = 0; k < nrows; ++k)
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c)
+                        if (c0 + c < (int)a.b_valid) a.out[(size_t)(r0 + k) * B + c0 + c] = tile[k * TS + c0 + c];
+            } else {
+                // transposed: RB lanes x 8 B contiguous of one seed's vector per store
+                constexpr int RB = Sh::RB;
+                const int k = lane % RB;
+                for (uint32_t b = lane / RB; b < a.b_valid; b += 32 / RB)
+                    if (k < nrows) a.out[(size_t)b * a.n + r0 + k] = tile[k * TS + b];
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            if (bl1[c] != 0.0) fx_add(fx[0][c], fx[1][c], bl1[c]);
+            if (bdm[c] != 0.0) fx_add(fx[2][c], fx[3][c], bdm[c]);
+        }
+        if (lane == 0 && !kLast) {
+            if (A.nz_out && nzw) atomicOr(A.nz_out + (r0 >> 5), nzw);
+            if (A.acc_valid && avw) atomicOr(A.acc_valid + (r0 >> 5), avw);
+        }
+        __syncwarp();
+    }
+
+    // residual / dangling mass: exact integer sums; the last CTA advances state
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int b = c0 + c;
+        if (fx[0][c] | fx[1][c]) fx_atomic_add(&s_fx[4 * b + 0], &s_fx[4 * b + 1], fx[0][c], fx[1][c]);
+        if (fx[2][c] | fx[3][c]) fx_atomic_add(&s_fx[4 * b + 2], &s_fx[4 * b + 3], fx[2][c], fx[3][c]);
+    }
+    __syncthreads();
+    for (int b = tid; b < B; b += Sh::NT) {
+        if (s_fx[4 * b + 0] | s_fx[4 * b + 1]) fx_atomic_add(&A.fx[4 * b + 0], &A.fx[4 * b + 1], s_fx[4 * b + 0], s_fx[4 * b + 1]);
+        if (s_fx[4 * b + 2] | s_fx[4 * b + 3]) fx_atomic_add(&A.fx[4 * b + 2], &A.fx[4 * b + 3], s_fx[4 * b + 2], s_fx[4 * b + 3]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_ticket = atomicAdd(a.done_cnt, 1u);
+    __syncthreads();
+    if (s_ticket != gridDim.x - 1) return;
+    __threadfence();
+    for (int b = tid; b < B; b += Sh::NT) {
+        ColState sc = a.state_in[b];
+        const unsigned long long h0 = atomicAdd(&A.fx[4 * b + 0], 0ull), l0 = atomicAdd(&A.fx[4 * b + 1], 0ull);
+        const unsigned long long h1 = atomicAdd(&A.fx[4 * b + 2], 0ull), l1 = atomicAdd(&A.fx[4 * b + 3], 0ull);
+        if (sc.active) {
+            const double res = fx_decode(h0, l0);
+            const double dm = fx_decode(h1, l1);
+            sc.residual = res;
+            sc.iters = a.step;
+            sc.converged = res < a.eps;
+            sc.active = !sc.converged && (a.terminal < 0 || (int64_t)a.step < a.terminal);
+            sc.has_spread = (a.policy == kUniform && dm != 0.0);
+            sc.spread = sc.has_spread ? ddiv(dmul(a.keep, dm), (double)a.n) : 0.0;
+        }
+        a.state_out[b] = sc;
+        A.fx[4 * b + 0] = A.fx[4 * b + 1] = A.fx[4 * b + 2] = A.fx[4 * b + 3] = 0ull;
+    }
+    if (tid == 0) {
+        *A.work_cnt = 0;
+        *a.done_cnt = 0;
+    }
+}
+
+}  // namespace tpa

@@ -1,0 +1,191 @@
+// cpi_spmv2.cuh -- K2 v2: the B = 1 sweep (PageRank / single-vector CPI).
+//
+// Same tiles and the same per-row arithmetic order as K2 v1 (cpi_kernels.cuh:
+// rows <= 32 nnz sequential per thread, longer rows a fixed warp tree, rows
+// above a tile one CTA tree), restructured for memory-level parallelism:
+//   * the tile's nnz range travels with the work item, so the index loads,
+//     the row_ptr loads and the per-row out-degree / accumulator loads are all
+//     issued at once (one round trip), then the gathers (a second one);
+//   * the L1 residual and dangling mass are reduced per CTA in a fixed tree
+//     and added across CTAs as exact 128-bit fixed-point integers (order-free),
+//     replacing v1's two-level ticket tree; the last CTA advances the state.
+#pragma once
+
+#include "cpi_spmm.cuh"
+
+namespace tpa {
+
+struct MvArgs {
+    StepArgs s;
+    const longlong2* __restrict__ item_nnz;  // [n_items] {nnz begin, nnz end}
+    unsigned long long* fx;                  // [4]: l1 hi/lo, dm hi/lo; zero between launches
+};
+
+__global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
+    const StepArgs& a = M.s;
+    __shared__ double s_vals[kMvTileNnz];
+    __shared__ int64_t s_rp[kMvTileRows + 1];
+    __shared__ double s_y[kMvTileRows];
+    __shared__ double s_red[kThreads];
+    __shared__ uint32_t s_ticket;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t item = blockIdx.x;
+    const ColState st = a.state_in[0];
+    const uint2 it = a.items[item];
+    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
+    const bool is_long = (it.y & kLongFlag) != 0;
+    const longlong2 nr = M.item_nnz[item];
+    const int64_t nb = nr.x, ne = nr.y;
+
+    if (!st.active) {
+        // column stopped earlier: only a pending combine remains (tpa.cpp:73)
+        if (a.out)
+            for (uint32_t v = rb + tid; v < re; v += kThreads) combine_only(a, v, 0, 1, v);
+        if (item == 0 && tid == 0) a.state_out[0] = st;
+        return;
+    }
+    const bool want_dm = a.policy == kUniform;
+    double my_l1 = 0.0, my_dm = 0.0;
+
+    if (!is_long) {
+        const uint32_t nrows = re - rb;
+        const int nnz = (int)(ne - nb);
+        constexpr int U = kMvTileNnz / kThreads;
+        constexpr int RPT = kMvTileRows / kThreads;  // rows per thread
+        // ---- round trip 1: indices, row pointers, degrees, accumulators ----
+        uint32_t u[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int k = tid + j * kThreads;
+            u[j] = k < nnz ? ld_stream_u32(a.col + nb + k) : 0u;
+        }
+        for (uint32_t r = tid; r <= nrows; r += kThreads) s_rp[r] = a.row_ptr[rb + r];
+        uint32_t dg[RPT];
+        double ac[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const uint32_t r = tid + q * kThreads;
+            dg[q] = r < nrows ? __ldg(a.deg + rb + r) : 0u;
+            ac[q] = (r < nrows && a.acc) ? a.acc[rb + r] : 0.0;
+        }
+        // ---- round trip 2: gathers ----
+        double v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int k = tid + j * kThreads;
+            v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int k = tid + j * kThreads;
+            if (k < nnz) s_vals[k] = v[j];
+        }
+        __syncthreads();
+        // short rows: one thread, ascending-source sequential sum (reference order)
+        for (uint32_t r = tid; r < nrows; r += kThreads) {
+            const int lo = (int)(s_rp[r] - nb), hi = (int)(s_rp[r + 1] - nb);
+            if (hi - lo <= kMvShortRow) {
+                double s = 0.0;
+                for (int k = lo; k < hi; ++k) s = dadd(s, s_vals[k]);
+                s_y[r] = s;
+            }
+        }
+        // longer rows of the tile: one warp each, lane-strided + butterfly
+        for (uint32_t base = warp * 32; base < nrows; base += kThreads) {
+            const uint32_t r = base + lane;
+            const int len = r < nrows ? (int)(s_rp[r + 1] - s_rp[r]) : 0;
+            unsigned mask = __ballot_sync(0xffffffffu, len > kMvShortRow);
+            while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const uint32_t rr = base + j;
+                const int lo = (int)(s_rp[rr] - nb), hi = (int)(s_rp[rr + 1] - nb);
+                double s = 0.0;
+                for (int k = lo + lane; k < hi; k += 32) s = dadd(s, s_vals[k]);
+                s = warp_sum(s);
+                if (lane == 0) s_y[rr] = s;
+            }
+        }
+        __syncthreads();
+        // epilogue with the prefetched degree / accumulator of each row
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const uint32_t r = tid + q * kThreads;
+            if (r >= nrows) continue;
+            const uint32_t vtx = rb + r;
+            double y = s_y[r];
+            if (st.has_spread) y = dadd(y, st.spread);  // graph.cpp:265-268
+            if (a.y_out) a.y_out[vtx] = y;
+            if (a.acc) {
+                const double f = dadd(ac[q], y);  // cpi.cpp:50
+                if (a.out) {
+                    a.out[vtx] = a.stranger ? dadd(dmul(a.scale, f), a.stranger[vtx]) : dmul(f, a.scale);
+                } else {
+                    a.acc[vtx] = f;
+                }
+            }
+            if (a.share_out) a.share_out[vtx] = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
+            my_l1 = dadd(my_l1, fabs(y));
+            if (want_dm && dg[q] == 0) my_dm = dadd(my_dm, y);
+        }
+    } else {
+        // one long row: every thread sums a fixed strided subset, then a fixed tree
+        double s = 0.0;
+        constexpr int U = 8;
+        int64_t e = nb + tid;
+        for (; e + (U - 1) * kThreads < ne; e += U * kThreads) {
+            uint32_t u[U];
+            double v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) u[j] = ld_stream_u32(a.col + e + j * kThreads);
+#pragma unroll
+            for (int j = 0; j < U; ++j) v[j] = __ldg(a.share_in + u[j]);
+#pragma unroll
+            for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
+        }
+        for (; e < ne; e += kThreads) s = dadd(s, __ldg(a.share_in + ld_stream_u32(a.col + e)));
+        s = block_sum(s, s_red);
+        if (tid == 0) {
+            const uint32_t d = __ldg(a.deg + rb);
+            const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
+            my_l1 = fabs(y);
+            if (want_dm && d == 0) my_dm = y;
+        }
+    }
+    // CTA partials (fixed tree) -> exact fixed-point totals across CTAs
+    const double l1 = block_sum(my_l1, s_red);
+    const double dm = want_dm ? block_sum(my_dm, s_red) : 0.0;
+    if (tid == 0) {
+        unsigned long long h = 0, l = 0;
+        if (l1 != 0.0) {
+            fx_add(h, l, l1);
+            fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
+        }
+        if (dm != 0.0) {
+            h = l = 0;
+            fx_add(h, l, dm);
+            fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
+        }
+        __threadfence();
+        s_ticket = atomicAdd(a.done_cnt, 1u);
+    }
+    __syncthreads();
+    if (s_ticket != gridDim.x - 1 || tid != 0) return;
+    __threadfence();
+    // last CTA: cpi.cpp:73-80, then reset the accumulators
+    ColState s = st;
+    const double res = fx_decode(atomicAdd(&M.fx[0], 0ull), atomicAdd(&M.fx[1], 0ull));
+    const double dmt = fx_decode(atomicAdd(&M.fx[2], 0ull), atomicAdd(&M.fx[3], 0ull));
+    s.residual = res;
+    s.iters = a.step;
+    s.converged = res < a.eps;
+    s.active = !s.converged && (a.terminal < 0 || (int64_t)a.step < a.terminal);
+    s.has_spread = (a.policy == kUniform && dmt != 0.0);
+    s.spread = s.has_spread ? ddiv(dmul(a.keep, dmt), (double)a.n) : 0.0;
+    a.state_out[0] = s;
+    M.fx[0] = M.fx[1] = M.fx[2] = M.fx[3] = 0ull;
+    *a.done_cnt = 0;
+}
+
+}  // namespace tpa

@@ -29,6 +29,8 @@
 #include "cpi_spmm.cuh"
 #include "cpi_spmm3.cuh"
 #include "cpi_spmm4.cuh"
+#include "cpi_spmm5.cuh"
+#include "cpi_spmv2.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
 
@@ -295,6 +297,7 @@ __global__ void k_acc_export(const double* __restrict__ src, const uint32_t* __r
 // ---------------------------------------------------------------------------
 struct Schedule {
     DevBuf items;
+    DevBuf item_nnz;  // {nnz begin, nnz end} per item (SpMV v2)
     uint32_t n_items = 0;
     uint32_t n_groups = 0;
 };
@@ -338,10 +341,31 @@ std::vector<uint2> build_items(const std::vector<int64_t>& rp, uint32_t n, int64
 static int spmm_version(int B) {
     static const int env = [] {
         const char* e = std::getenv("TPA_SPMM");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : 5;
     }();
     if (B != 32 && B != 64) return 2;
-    return env == 2 || env == 3 ? env : 4;
+    return (env >= 2 && env <= 4) ? env : 5;
+}
+
+template <int B, bool L>
+static int mm5_occupancy() {
+    const size_t dyn = Mm5<B>::kDynSmem;
+    CK(cudaFuncSetAttribute(k_mm_fused<B, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mm_fused<B, L>, Mm5<B>::NT, dyn));
+    return std::max(occ, 1);
+}
+
+// Sweeps (of a seed batch) run frontier-driven: push-mark then pull.
+constexpr uint32_t kSparseSweeps = 3;
+
+// SpMV generation: v2 (prefetched tiles, fixed-point residual) unless TPA_SPMV=1.
+static int spmv_version() {
+    static const int env = [] {
+        const char* e = std::getenv("TPA_SPMV");
+        return e ? std::atoi(e) : 2;
+    }();
+    return env == 1 ? 1 : 2;
 }
 
 template <int B>
@@ -384,7 +408,9 @@ struct Workspace {
     DevBuf nz[2], acc_valid, long_cnt, seg_part, work_cnt, fx;
     int grid = 0;  // persistent grid of k_step_spmm2<B>
     DevBuf Y, ybits;  // v4: row sums and their written-rows bitmap
+    DevBuf rowflag, sparse_ctl;  // v4 sparse sweeps: reachable rows; {cost, dense}
     int grid_gather = 0, grid_epi = 0;
+    int grid_fused[2] = {0, 0};  // v5: mid / last sweep
 };
 
 // Long rows of CSR(Ãᵀ) (in-degree > kLong) cut into kLong-nnz segments, the
@@ -392,7 +418,9 @@ struct Workspace {
 struct LongRows {
     DevBuf seg_row, seg_lo, seg_long, long_first, long_nseg;
     uint32_t n_segs = 0, n_long = 0;
-    DevBuf blocks;  // short-row blocks {first row, rows}
+    DevBuf blocks;  // short-row blocks {first row, rows} (kMmRows windows)
+    DevBuf blocks8; // the same inside 8-row windows (v5 at B = 64)
+    uint32_t n_blocks8 = 0;
 };
 
 }  // namespace tpa
@@ -408,6 +436,7 @@ struct tpa_graph {
     int policy = 0;
     uint64_t fingerprint = 0;
     DevBuf row_ptr, col, deg;
+    DevBuf out_off, out_tgt;  // the out-edge CSR itself (frontier push-marking)
     Schedule mv;  // SpMV work items
     LongRows longs;
     uint32_t n_blocks = 0;  // kMmRows-row blocks
@@ -418,6 +447,7 @@ struct tpa_graph {
     uint64_t launches = 0;
     int num_sms = 148;
     std::mutex mu;
+    bool sparse_off = std::getenv("TPA_NO_SPARSE") != nullptr;  // A/B switch
     // optional per-sweep-kernel CUDA-event timing (bench instrumentation)
     bool profile = false;
     struct ProfEvent {
@@ -468,6 +498,10 @@ struct tpa_graph {
             CK(cudaMemsetAsync(w.done_cnt.p, 0, w.done_cnt.bytes, stream));
         }
         w.state.ensure(2 * (size_t)B * sizeof(ColState), stream);
+        if (B == 1 && !w.fx.p) {
+            w.fx.ensure(4 * 8, stream);
+            CK(cudaMemsetAsync(w.fx.p, 0, w.fx.bytes, stream));
+        }
         if (B > 1 && !w.work_cnt.p) {
             const size_t words = ((size_t)n + 31) / 32 + 1;
             w.nz[0].ensure(words * 4, stream);
@@ -488,9 +522,19 @@ struct tpa_graph {
                 case 64: occ = mm_occupancy<64>(); break;
             }
             w.grid = std::max(1, occ) * num_sms;
-            if (spmm_version(B) == 4) {
+            if (spmm_version(B) >= 4) {
+                if (B == 32) {
+                    w.grid_fused[0] = mm5_occupancy<32, false>() * num_sms;
+                    w.grid_fused[1] = mm5_occupancy<32, true>() * num_sms;
+                }
+                if (B == 64) {
+                    w.grid_fused[0] = mm5_occupancy<64, false>() * num_sms;
+                    w.grid_fused[1] = mm5_occupancy<64, true>() * num_sms;
+                }
                 w.Y.ensure((size_t)n * B * 8, stream);
                 w.ybits.ensure(words * 4, stream);
+                w.rowflag.ensure((size_t)n + 16, stream);
+                w.sparse_ctl.ensure(16, stream);
                 if (B == 32) mm4_grids<32>(num_sms, w.grid_gather, w.grid_epi);
                 if (B == 64) mm4_grids<64>(num_sms, w.grid_gather, w.grid_epi);
             }
@@ -601,11 +645,43 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         e1 = g->take_event();
         CK(cudaEventRecord(e0, g->stream));
     }
-    const bool v4 = B > 1 && spmm_version(B) == 4;
+    const bool v4 = B > 1 && spmm_version(B) >= 4;
     if (v4) {
-        Mm4Args P{*mm, w.Y.as<double>(), w.ybits.as<uint32_t>()};
+        Mm4Args P{*mm, w.Y.as<double>(), w.ybits.as<uint32_t>(), nullptr, nullptr,
+                  B == 64 ? g->longs.blocks8.as<uint2>() : g->longs.blocks.as<uint2>(),
+                  B == 64 ? g->longs.n_blocks8 : g->n_blocks};
         CK(cudaMemsetAsync(w.ybits.p, 0, w.ybits.bytes, g->stream));
-        if (B == 32) {
+        // the first sweeps of a seed batch usually see a small frontier: if it
+        // pushes along at most m/32 edges, mark the rows it reaches (push over
+        // the out-CSR) and pull only those; the decision is taken on the device
+        if (mm->nz_in && a.step <= kSparseSweeps && !g->sparse_off) {
+            const uint32_t words = (g->n + 31) / 32;
+            auto* ctl = w.sparse_ctl.as<unsigned long long>();
+            CK(cudaMemsetAsync(w.sparse_ctl.p, 0, 16, g->stream));
+            CK(cudaMemsetAsync(w.rowflag.p, 0, g->n, g->stream));
+            const int gb = grid_for(words, 8, 16 * g->num_sms);
+            k_frontier_cost<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(), ctl);
+            CKL("k_frontier_cost");
+            k_mark_out<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(),
+                                                  g->out_tgt.as<uint32_t>(), ctl, g->m / 32,
+                                                  w.rowflag.as<uint8_t>(), reinterpret_cast<int*>(ctl + 1));
+            CKL("k_mark_out");
+            g->launches += 2;
+            P.rowflag = w.rowflag.as<uint8_t>();
+            P.dense = reinterpret_cast<const int*>(ctl + 1);
+        }
+        if (spmm_version(B) == 5) {
+            const bool last = a.out != nullptr;
+            const int gr = w.grid_fused[last ? 1 : 0];
+            if (B == 32) {
+                if (last) k_mm_fused<32, true><<<gr, Mm5<32>::NT, Mm5<32>::kDynSmem, g->stream>>>(P);
+                else k_mm_fused<32, false><<<gr, Mm5<32>::NT, Mm5<32>::kDynSmem, g->stream>>>(P);
+            } else {
+                if (last) k_mm_fused<64, true><<<gr, Mm5<64>::NT, Mm5<64>::kDynSmem, g->stream>>>(P);
+                else k_mm_fused<64, false><<<gr, Mm5<64>::NT, Mm5<64>::kDynSmem, g->stream>>>(P);
+            }
+            g->launches -= 1;  // one kernel (the common ++ below counts it)
+        } else if (B == 32) {
             k_mm_gather<32><<<w.grid_gather, Mm4<32>::NT, 0, g->stream>>>(P);
             CKL("k_mm_gather<32>");
             k_mm_epi<32><<<w.grid_epi, Mm4<32>::NT, mm4_epi_smem<32>(), g->stream>>>(P);
@@ -614,9 +690,14 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             CKL("k_mm_gather<64>");
             k_mm_epi<64><<<w.grid_epi, Mm4<64>::NT, mm4_epi_smem<64>(), g->stream>>>(P);
         }
-        g->launches += 1;
+        g->launches += 1;  // + the epilogue below
     } else switch (B) {
-        case 1: k_step_spmv<<<grid, block, 0, g->stream>>>(a); break;
+        case 1:
+            if (spmv_version() == 2)
+                k_step_spmv2<<<grid, block, 0, g->stream>>>(MvArgs{a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>()});
+            else
+                k_step_spmv<<<grid, block, 0, g->stream>>>(a);
+            break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
         case 16: k_step_spmm2<16><<<grid, MmShape<16>::NT, MmShape<16>::kDynSmem, g->stream>>>(*mm); break;
         case 32:
@@ -952,6 +1033,11 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
                                                end_bit, s));
         }
         k_row_ptr<<<blocks, 256, 0, s>>>(d_keys.as<uint32_t>(), m, n, g->row_ptr.as<int64_t>());
+        // keep the out-edge CSR (frontier push-marking of sparse sweeps)
+        g->out_off.ensure((n + 1ull) * 8, g->stream);
+        g->out_tgt.ensure(std::max<uint64_t>(m, 1) * 4, g->stream);
+        CK(cudaMemcpyAsync(g->out_off.p, out_offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
+        if (m) CK(cudaMemcpyAsync(g->out_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
         CKL("k_row_ptr");
         std::vector<int64_t> rp(n + 1ull);
         CK(cudaMemcpyAsync(rp.data(), g->row_ptr.p, (n + 1ull) * 8, cudaMemcpyDeviceToHost, s));
@@ -992,28 +1078,35 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
             put(L.long_first, long_first.data(), long_first.size() * 4);
             put(L.long_nseg, long_nseg.data(), long_nseg.size() * 4);
             // short-row blocks: consecutive short rows inside one aligned
-            // kMmRows window, at most kBlockNnz nnz (a lone row may reach kLong)
-            std::vector<uint2> blocks;
-            for (uint32_t w0 = 0; w0 < n; w0 += kMmRows) {
-                const uint32_t w1 = std::min<uint32_t>(n, w0 + kMmRows);
-                uint32_t r = w0;
-                while (r < w1) {
-                    if (rp[r + 1] - rp[r] > kLong) {
-                        ++r;
-                        continue;
+            // window, at most kBlockNnz nnz (a lone row may reach kLong)
+            auto make_blocks = [&](uint32_t win) {
+                std::vector<uint2> blocks;
+                for (uint32_t w0 = 0; w0 < n; w0 += win) {
+                    const uint32_t w1 = std::min<uint32_t>(n, w0 + win);
+                    uint32_t r = w0;
+                    while (r < w1) {
+                        if (rp[r + 1] - rp[r] > kLong) {
+                            ++r;
+                            continue;
+                        }
+                        const uint32_t b0 = r;
+                        int64_t nnz = 0;
+                        while (r < w1 && rp[r + 1] - rp[r] <= kLong) {
+                            const int64_t L2 = rp[r + 1] - rp[r];
+                            if (r > b0 && nnz + L2 > kBlockNnz) break;
+                            nnz += L2;
+                            ++r;
+                        }
+                        blocks.push_back(make_uint2(b0, r - b0));
                     }
-                    const uint32_t b0 = r;
-                    int64_t nnz = 0;
-                    while (r < w1 && rp[r + 1] - rp[r] <= kLong) {
-                        const int64_t L2 = rp[r + 1] - rp[r];
-                        if (r > b0 && nnz + L2 > kBlockNnz) break;
-                        nnz += L2;
-                        ++r;
-                    }
-                    blocks.push_back(make_uint2(b0, r - b0));
                 }
-            }
+                return blocks;
+            };
+            std::vector<uint2> blocks = make_blocks(kMmRows);
             put(L.blocks, blocks.data(), blocks.size() * sizeof(uint2));
+            std::vector<uint2> blocks8 = make_blocks(8);
+            put(L.blocks8, blocks8.data(), blocks8.size() * sizeof(uint2));
+            L.n_blocks8 = (uint32_t)blocks8.size();
             g->n_blocks = (uint32_t)blocks.size();
             CK(cudaStreamSynchronize(s));
         }
@@ -1021,6 +1114,16 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         g->mv.n_groups = (g->mv.n_items + kGroupItems - 1) / kGroupItems;
         g->mv.items.ensure(mv.size() * sizeof(uint2), g->stream);
         CK(cudaMemcpyAsync(g->mv.items.p, mv.data(), mv.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+        {
+            std::vector<longlong2> nr(mv.size());
+            for (size_t i = 0; i < mv.size(); ++i) {
+                const uint32_t rb = mv[i].x, re = mv[i].y & ~kLongFlag;
+                nr[i] = make_longlong2(rp[rb], rp[re]);
+            }
+            g->mv.item_nnz.ensure(nr.size() * sizeof(longlong2), g->stream);
+            CK(cudaMemcpyAsync(g->mv.item_nnz.p, nr.data(), nr.size() * sizeof(longlong2), cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        }
         CK(cudaStreamSynchronize(s));
         *out = g.release();
     });
@@ -1037,9 +1140,12 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->row_ptr.release();
             g->col.release();
             g->deg.release();
+            g->out_off.release();
+            g->out_tgt.release();
             g->mv.items.release();
+            g->mv.item_nnz.release();
             for (DevBuf* d : {&g->longs.seg_row, &g->longs.seg_lo, &g->longs.seg_long, &g->longs.long_first,
-                              &g->longs.long_nseg, &g->longs.blocks})
+                              &g->longs.long_nseg, &g->longs.blocks, &g->longs.blocks8})
                 d->release();
             g->init_part.release();
             g->out_stage.release();
