@@ -370,8 +370,9 @@ def run_ours(args):
         # dominant kernel: the SpMM sweep.  Roofline on its densest launch, the
         # last family sweep x^(S-1) (fused combine), with that sweep's exact
         # compulsory bytes; the sparse early sweeps are listed per index.
-        kname = (f"k_mm_gather<{Bk}> + k_mm_epi<{Bk}>" if Bk in (32, 64) and os.environ.get("TPA_SPMM", "4") == "4"
-                 else f"k_step_spmm2<{Bk}>")
+        ver = os.environ.get("TPA_SPMM", "5") if Bk in (32, 64) else "2"
+        kname = {"5": f"k_mm_fused<{Bk}>", "4": f"k_mm_gather<{Bk}> + k_mm_epi<{Bk}>",
+                 "3": f"k_step_spmm3<{Bk}>"}.get(ver, f"k_step_spmm2<{Bk}>")
         last = per_sweep.get(S - 1)
         bytes_launch = sweep_bytes(n, m, Bk, "last")
         avg_ms = last["avg_ms"] if last else mm_ms / mm_cnt

@@ -18,12 +18,17 @@
 
 namespace tpa {
 
-template <int B>
+#ifndef TPA_MM5_MINB
+#define TPA_MM5_MINB 8
+#endif
+
+template <int B, int RB_>
 struct Mm5 {
     static_assert(B == 32 || B == 64, "v5: one warp per row group");
+    static_assert(RB_ == 4 || RB_ == 8 || RB_ == 16, "rows per block");
     static constexpr int CPL = B / 32;
     static constexpr int U = 16 / CPL;         // gathers in flight per lane
-    static constexpr int RB = B == 32 ? 16 : 8;  // rows per block (smem per warp ~8 KiB)
+    static constexpr int RB = RB_;             // rows per block (the host's block window)
     static constexpr int NW = 4;               // warps per CTA
     static constexpr int NT = NW * 32;
     static constexpr int TS = B + 2;           // padded row stride (doubles) of the tile
@@ -42,9 +47,9 @@ __device__ __forceinline__ void cp_async_acc(double* dst_smem, const double* src
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
 }
 
-template <int B, bool kLast>
-__global__ void __launch_bounds__(Mm5<B>::NT, 8) k_mm_fused(Mm4Args P) {
-    using Sh = Mm5<B>;
+template <int B, bool kLast, int RB>
+__global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Args P) {
+    using Sh = Mm5<B, RB>;
     constexpr int CPL = Sh::CPL, U = Sh::U, TS = Sh::TS;
     const MmArgs& A = P.m;
     const StepArgs& a = A.s;
@@ -295,7 +300,6 @@ __global__ void __launch_bounds__(Mm5<B>::NT, 8) k_mm_fused(Mm4Args P) {
                         if (c0 + c < (int)a.b_valid) a.out[(size_t)(r0 + k) * B + c0 + c] = tile[k * TS + c0 + c];
             } else {
                 // transposed: RB lanes x 8 B contiguous of one seed's vector per store
-                constexpr int RB = Sh::RB;
                 const int k = lane % RB;
                 for (uint32_t b = lane / RB; b < a.b_valid; b += 32 / RB)
                     if (k < nrows) a.out[(size_t)b * a.n + r0 + k] = tile[k * TS + b];

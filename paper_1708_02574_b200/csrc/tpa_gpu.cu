@@ -347,13 +347,39 @@ static int spmm_version(int B) {
     return (env >= 2 && env <= 4) ? env : 5;
 }
 
+// v5 rows per block: B = 32 pulls its first sweep (a small frontier: few
+// blocks live) in 16-row blocks and the dense ones in 8-row blocks (half the
+// shared memory per warp: 32 instead of 24 resident warps per SM); B = 64 in
+// 8-row blocks.  TPA_MM5_RB=4/8/16 forces one size (A/B experiments).
+static int mm5_rows(int B, uint32_t step) {
+    static const int env = [] {
+        const char* e = std::getenv("TPA_MM5_RB");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 4 || v == 8 || v == 16) ? v : 0;
+    }();
+    if (env) return env;
+    if (B == 32) return step <= 1 ? 16 : 8;
+    return 8;
+}
+
+template <int B, bool L, int RB>
+static void launch_fused(const Mm4Args& P, int num_sms, cudaStream_t stream) {
+    using Sh = Mm5<B, RB>;
+    static const int grid = [num_sms] {
+        CK(cudaFuncSetAttribute(k_mm_fused<B, L, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Sh::kDynSmem));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mm_fused<B, L, RB>, Sh::NT, Sh::kDynSmem));
+        return std::max(occ, 1) * num_sms;
+    }();
+    k_mm_fused<B, L, RB><<<grid, Sh::NT, Sh::kDynSmem, stream>>>(P);
+}
+
 template <int B, bool L>
-static int mm5_occupancy() {
-    const size_t dyn = Mm5<B>::kDynSmem;
-    CK(cudaFuncSetAttribute(k_mm_fused<B, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mm_fused<B, L>, Mm5<B>::NT, dyn));
-    return std::max(occ, 1);
+static void launch_fused_rb(const Mm4Args& P, int rb, int num_sms, cudaStream_t stream) {
+    if (rb == 4) launch_fused<B, L, 4>(P, num_sms, stream);
+    else if (rb == 8) launch_fused<B, L, 8>(P, num_sms, stream);
+    else launch_fused<B, L, 16>(P, num_sms, stream);
 }
 
 // Sweeps (of a seed batch) run frontier-driven: push-mark then pull.
@@ -410,7 +436,6 @@ struct Workspace {
     DevBuf Y, ybits;  // v4: row sums and their written-rows bitmap
     DevBuf rowflag, sparse_ctl;  // v4 sparse sweeps: reachable rows; {cost, dense}
     int grid_gather = 0, grid_epi = 0;
-    int grid_fused[2] = {0, 0};  // v5: mid / last sweep
 };
 
 // Long rows of CSR(Ãᵀ) (in-degree > kLong) cut into kLong-nnz segments, the
@@ -419,8 +444,9 @@ struct LongRows {
     DevBuf seg_row, seg_lo, seg_long, long_first, long_nseg;
     uint32_t n_segs = 0, n_long = 0;
     DevBuf blocks;  // short-row blocks {first row, rows} (kMmRows windows)
-    DevBuf blocks8; // the same inside 8-row windows (v5 at B = 64)
-    uint32_t n_blocks8 = 0;
+    DevBuf blocks_w[3];  // the same inside 4 / 8 / 16-row windows (v5)
+    uint32_t n_blocks_w[3] = {0, 0, 0};
+    static int wi(int rows) { return rows == 4 ? 0 : rows == 8 ? 1 : 2; }
 };
 
 }  // namespace tpa
@@ -523,14 +549,6 @@ struct tpa_graph {
             }
             w.grid = std::max(1, occ) * num_sms;
             if (spmm_version(B) >= 4) {
-                if (B == 32) {
-                    w.grid_fused[0] = mm5_occupancy<32, false>() * num_sms;
-                    w.grid_fused[1] = mm5_occupancy<32, true>() * num_sms;
-                }
-                if (B == 64) {
-                    w.grid_fused[0] = mm5_occupancy<64, false>() * num_sms;
-                    w.grid_fused[1] = mm5_occupancy<64, true>() * num_sms;
-                }
                 w.Y.ensure((size_t)n * B * 8, stream);
                 w.ybits.ensure(words * 4, stream);
                 w.rowflag.ensure((size_t)n + 16, stream);
@@ -646,10 +664,10 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         CK(cudaEventRecord(e0, g->stream));
     }
     const bool v4 = B > 1 && spmm_version(B) >= 4;
+    const int rb = spmm_version(B) == 5 ? mm5_rows(B, a.step) : (B == 64 ? 8 : 16);
     if (v4) {
         Mm4Args P{*mm, w.Y.as<double>(), w.ybits.as<uint32_t>(), nullptr, nullptr,
-                  B == 64 ? g->longs.blocks8.as<uint2>() : g->longs.blocks.as<uint2>(),
-                  B == 64 ? g->longs.n_blocks8 : g->n_blocks};
+                  g->longs.blocks_w[LongRows::wi(rb)].as<uint2>(), g->longs.n_blocks_w[LongRows::wi(rb)]};
         CK(cudaMemsetAsync(w.ybits.p, 0, w.ybits.bytes, g->stream));
         // the first sweeps of a seed batch usually see a small frontier: if it
         // pushes along at most m/32 edges, mark the rows it reaches (push over
@@ -672,13 +690,12 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         }
         if (spmm_version(B) == 5) {
             const bool last = a.out != nullptr;
-            const int gr = w.grid_fused[last ? 1 : 0];
             if (B == 32) {
-                if (last) k_mm_fused<32, true><<<gr, Mm5<32>::NT, Mm5<32>::kDynSmem, g->stream>>>(P);
-                else k_mm_fused<32, false><<<gr, Mm5<32>::NT, Mm5<32>::kDynSmem, g->stream>>>(P);
+                if (last) launch_fused_rb<32, true>(P, rb, g->num_sms, g->stream);
+                else launch_fused_rb<32, false>(P, rb, g->num_sms, g->stream);
             } else {
-                if (last) k_mm_fused<64, true><<<gr, Mm5<64>::NT, Mm5<64>::kDynSmem, g->stream>>>(P);
-                else k_mm_fused<64, false><<<gr, Mm5<64>::NT, Mm5<64>::kDynSmem, g->stream>>>(P);
+                if (last) launch_fused_rb<64, true>(P, rb, g->num_sms, g->stream);
+                else launch_fused_rb<64, false>(P, rb, g->num_sms, g->stream);
             }
             g->launches -= 1;  // one kernel (the common ++ below counts it)
         } else if (B == 32) {
@@ -1104,9 +1121,11 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
             };
             std::vector<uint2> blocks = make_blocks(kMmRows);
             put(L.blocks, blocks.data(), blocks.size() * sizeof(uint2));
-            std::vector<uint2> blocks8 = make_blocks(8);
-            put(L.blocks8, blocks8.data(), blocks8.size() * sizeof(uint2));
-            L.n_blocks8 = (uint32_t)blocks8.size();
+            for (int rows : {4, 8, 16}) {
+                std::vector<uint2> bw = make_blocks(rows);
+                put(L.blocks_w[LongRows::wi(rows)], bw.data(), bw.size() * sizeof(uint2));
+                L.n_blocks_w[LongRows::wi(rows)] = (uint32_t)bw.size();
+            }
             g->n_blocks = (uint32_t)blocks.size();
             CK(cudaStreamSynchronize(s));
         }
@@ -1145,7 +1164,8 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->mv.items.release();
             g->mv.item_nnz.release();
             for (DevBuf* d : {&g->longs.seg_row, &g->longs.seg_lo, &g->longs.seg_long, &g->longs.long_first,
-                              &g->longs.long_nseg, &g->longs.blocks, &g->longs.blocks8})
+                              &g->longs.long_nseg, &g->longs.blocks, &g->longs.blocks_w[0],
+                              &g->longs.blocks_w[1], &g->longs.blocks_w[2]})
                 d->release();
             g->init_part.release();
             g->out_stage.release();

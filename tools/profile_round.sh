@@ -9,5 +9,5 @@ $CMD > gpurun_out/ll_plain.json 2> gpurun_out/ll_plain.err && \
   ncu --metrics gpu__time_duration.sum --clock-control none -s 846 -c 300 --csv \
       --log-file gpurun_out/launches.csv $CMD > gpurun_out/ll_ncu.log 2>&1; echo "launch list rc $?"
 python tools/profile_step.py > gpurun_out/ps_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_step" -s 117 -c 4 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_step_spmv2|k_mm_fused" -s 116 -c 5 \
       -o gpurun_out/prof_full python tools/profile_step.py > gpurun_out/ps_ncu.log 2>&1; echo "full rc $?"
