@@ -268,8 +268,7 @@ __global__ void __launch_bounds__(Mm3Shape<B>::NT) k_step_spmm3(MmArgs A) {
             const uint32_t f0 = A.long_first[li], ns = A.long_nseg[li];
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                double y = __ldcg(A.seg_part + (size_t)f0 * B + c0 + c);
-                for (uint32_t j = 1; j < ns; ++j) y = dadd(y, __ldcg(A.seg_part + (size_t)(f0 + j) * B + c0 + c));
+                const double y = seg_sum(A.seg_part + (size_t)f0 * B + c0 + c, B, ns);
                 yb[0][c0 + c] = y;
             }
             if (lane == 0) A.long_cnt[li] = 0;

@@ -84,24 +84,47 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     const uint32_t* __restrict__ col = a.col;
     const uint32_t* __restrict__ nz = A.nz_in;
     const double* __restrict__ share = a.share_in;
-    const uint32_t total = A.n_segs + P.n_blocks_rb;
     const bool use_mask = P.rowflag != nullptr && *P.dense == 0;
+    // sparse sweep: the items are the long-row segments + the marked windows
+    const bool by_window = use_mask && P.wl != nullptr;
+    const uint32_t n_seg_items = by_window ? *P.sl_cnt : A.n_segs;
+    const uint32_t total = n_seg_items + (by_window ? *P.wl_cnt : P.n_blocks_rb);
     const bool work = any_active || kLast;
 
-    uint32_t next_item = 0;
-    if (work && lane == 0) next_item = atomicAdd(A.work_cnt, 1u);
+    // first item by warp id, later ones from the shared counter (offset by the
+    // warp count): a sparse sweep with fewer items than warps costs no atomics
+    const uint32_t n_warps = gridDim.x * Sh::NW;
+    uint32_t next_item = blockIdx.x * Sh::NW + wid;
+    uint32_t pb = 0, pe = 0;  // blocks of the current window still to do (warp-uniform)
     while (work) {
-        const uint32_t item = __shfl_sync(0xffffffffu, next_item, 0);
-        if (item >= total) break;
-        if (lane == 0) next_item = atomicAdd(A.work_cnt, 1u);
-        const bool is_seg = item < A.n_segs;
+        uint32_t item = 0;
+        bool is_seg = false;
+        if (pb >= pe) {
+            item = __shfl_sync(0xffffffffu, next_item, 0);
+            if (item >= total) break;
+            if (lane == 0) next_item = n_warps + atomicAdd(A.work_cnt, 1u);
+            is_seg = item < n_seg_items;
+            if (is_seg) {
+                if (by_window) item = P.sl[item];  // -> segment id
+            } else {
+                if (by_window) {
+                    const uint32_t wdx = P.wl[item - n_seg_items];
+                    pb = P.win_blk[wdx];
+                    pe = P.win_blk[wdx + 1];
+                    if (pb >= pe) continue;
+                } else {
+                    pb = item - A.n_segs;
+                    pe = pb + 1;
+                }
+            }
+        }
         uint32_t r0;
         int nrows;
         if (is_seg) {
             r0 = A.seg_row[item];
             nrows = 1;
         } else {
-            const uint2 blk = P.blocks_rb[item - A.n_segs];
+            const uint2 blk = P.blocks_rb[pb++];
             r0 = blk.x;
             nrows = (int)blk.y;
         }
@@ -235,8 +258,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             const uint32_t f0 = A.long_first[li], ns = A.long_nseg[li];
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                double y = __ldcg(A.seg_part + (size_t)f0 * B + c0 + c);
-                for (uint32_t j = 1; j < ns; ++j) y = dadd(y, __ldcg(A.seg_part + (size_t)(f0 + j) * B + c0 + c));
+                const double y = seg_sum(A.seg_part + (size_t)f0 * B + c0 + c, B, ns);
                 yb[0][c0 + c] = y;
             }
             if (lane == 0) A.long_cnt[li] = 0;

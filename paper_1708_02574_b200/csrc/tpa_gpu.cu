@@ -30,7 +30,7 @@
 #include "cpi_spmm3.cuh"
 #include "cpi_spmm4.cuh"
 #include "cpi_spmm5.cuh"
-#include "cpi_spmv2.cuh"
+#include "cpi_spmv3.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
 
@@ -385,13 +385,16 @@ static void launch_fused_rb(const Mm4Args& P, int rb, int num_sms, cudaStream_t 
 // Sweeps (of a seed batch) run frontier-driven: push-mark then pull.
 constexpr uint32_t kSparseSweeps = 3;
 
-// SpMV generation: v2 (prefetched tiles, fixed-point residual) unless TPA_SPMV=1.
+// SpMV generation: v2 (prefetched tiles, fixed-point residual); TPA_SPMV=1
+// selects v1, TPA_SPMV=3 the warp-independent v3 (measured slower: the B200's
+// L1 sustains ~1 random 8-byte gather/clk/SM, tools/gather8_micro.cu, and v3's
+// per-row shared-memory walk adds to the same pipe).
 static int spmv_version() {
     static const int env = [] {
         const char* e = std::getenv("TPA_SPMV");
         return e ? std::atoi(e) : 2;
     }();
-    return env == 1 ? 1 : 2;
+    return (env == 1 || env == 3) ? env : 2;
 }
 
 template <int B>
@@ -434,7 +437,10 @@ struct Workspace {
     DevBuf nz[2], acc_valid, long_cnt, seg_part, work_cnt, fx;
     int grid = 0;  // persistent grid of k_step_spmm2<B>
     DevBuf Y, ybits;  // v4: row sums and their written-rows bitmap
-    DevBuf rowflag, sparse_ctl;  // v4 sparse sweeps: reachable rows; {cost, dense}
+    DevBuf rowflag, sparse_ctl;  // sparse sweeps: reachable rows; {cost, dense, window count}
+    DevBuf wbits, wl;            // sparse sweeps: marked windows (bitmap, list)
+    DevBuf big;                  // sparse sweeps: edge chunks of high out-degree frontier rows
+    DevBuf sl;                   // sparse sweeps: segments of the marked long rows
     int grid_gather = 0, grid_epi = 0;
 };
 
@@ -444,9 +450,10 @@ struct LongRows {
     DevBuf seg_row, seg_lo, seg_long, long_first, long_nseg;
     uint32_t n_segs = 0, n_long = 0;
     DevBuf blocks;  // short-row blocks {first row, rows} (kMmRows windows)
-    DevBuf blocks_w[3];  // the same inside 4 / 8 / 16-row windows (v5)
-    uint32_t n_blocks_w[3] = {0, 0, 0};
-    static int wi(int rows) { return rows == 4 ? 0 : rows == 8 ? 1 : 2; }
+    DevBuf blocks_w[4];  // the same inside 4 / 8 / 16 / 32-row windows (SpMM v5, SpMV v3)
+    uint32_t n_blocks_w[4] = {0, 0, 0, 0};
+    DevBuf win_blk_w[4];  // per window: index of its first block (n_windows + 1 entries)
+    static int wi(int rows) { return rows == 4 ? 0 : rows == 8 ? 1 : rows == 16 ? 2 : 3; }
 };
 
 }  // namespace tpa
@@ -474,6 +481,12 @@ struct tpa_graph {
     int num_sms = 148;
     std::mutex mu;
     bool sparse_off = std::getenv("TPA_NO_SPARSE") != nullptr;  // A/B switch
+    bool no_window_list = std::getenv("TPA_NO_WINDOW_LIST") != nullptr;  // A/B switch
+    uint64_t sparse_div = [] {  // sparse sweep if the push touches <= m / sparse_div edges
+        const char* e = std::getenv("TPA_SPARSE_DIV");
+        const long v = e ? std::atol(e) : 32;
+        return (uint64_t)(v > 0 ? v : 32);
+    }();
     // optional per-sweep-kernel CUDA-event timing (bench instrumentation)
     bool profile = false;
     struct ProfEvent {
@@ -527,6 +540,9 @@ struct tpa_graph {
         if (B == 1 && !w.fx.p) {
             w.fx.ensure(4 * 8, stream);
             CK(cudaMemsetAsync(w.fx.p, 0, w.fx.bytes, stream));
+            w.long_cnt.ensure((size_t)std::max<uint32_t>(longs.n_long, 1) * 4, stream);
+            w.seg_part.ensure((size_t)std::max<uint32_t>(longs.n_segs, 1) * 8, stream);
+            CK(cudaMemsetAsync(w.long_cnt.p, 0, w.long_cnt.bytes, stream));
         }
         if (B > 1 && !w.work_cnt.p) {
             const size_t words = ((size_t)n + 31) / 32 + 1;
@@ -552,7 +568,11 @@ struct tpa_graph {
                 w.Y.ensure((size_t)n * B * 8, stream);
                 w.ybits.ensure(words * 4, stream);
                 w.rowflag.ensure((size_t)n + 16, stream);
-                w.sparse_ctl.ensure(16, stream);
+                w.sparse_ctl.ensure(32, stream);
+                w.big.ensure(mark_chunk_cap(m) * sizeof(ulonglong2), stream);
+                w.sl.ensure(((size_t)longs.n_segs + 1) * 4, stream);
+                w.wbits.ensure(((size_t)n / 4 / 32 + 2) * 4, stream);
+                w.wl.ensure(((size_t)n / 4 + 2) * 4, stream);
                 if (B == 32) mm4_grids<32>(num_sms, w.grid_gather, w.grid_epi);
                 if (B == 64) mm4_grids<64>(num_sms, w.grid_gather, w.grid_epi);
             }
@@ -668,25 +688,48 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
     if (v4) {
         Mm4Args P{*mm, w.Y.as<double>(), w.ybits.as<uint32_t>(), nullptr, nullptr,
                   g->longs.blocks_w[LongRows::wi(rb)].as<uint2>(), g->longs.n_blocks_w[LongRows::wi(rb)]};
-        CK(cudaMemsetAsync(w.ybits.p, 0, w.ybits.bytes, g->stream));
+        if (spmm_version(B) == 4) CK(cudaMemsetAsync(w.ybits.p, 0, w.ybits.bytes, g->stream));
         // the first sweeps of a seed batch usually see a small frontier: if it
         // pushes along at most m/32 edges, mark the rows it reaches (push over
         // the out-CSR) and pull only those; the decision is taken on the device
         if (mm->nz_in && a.step <= kSparseSweeps && !g->sparse_off) {
             const uint32_t words = (g->n + 31) / 32;
             auto* ctl = w.sparse_ctl.as<unsigned long long>();
-            CK(cudaMemsetAsync(w.sparse_ctl.p, 0, 16, g->stream));
+            CK(cudaMemsetAsync(w.sparse_ctl.p, 0, 32, g->stream));
             CK(cudaMemsetAsync(w.rowflag.p, 0, g->n, g->stream));
+            const bool by_win = spmm_version(B) == 5 && !g->no_window_list;
+            const int rb_shift = rb == 4 ? 2 : rb == 8 ? 3 : rb == 16 ? 4 : 5;
+            if (by_win) CK(cudaMemsetAsync(w.wbits.p, 0, ((size_t)(g->n >> rb_shift) / 32 + 1) * 4, g->stream));
+            uint32_t* wl_cnt = reinterpret_cast<uint32_t*>(w.sparse_ctl.as<char>() + 12);
             const int gb = grid_for(words, 8, 16 * g->num_sms);
             k_frontier_cost<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(), ctl);
             CKL("k_frontier_cost");
-            k_mark_out<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(),
-                                                  g->out_tgt.as<uint32_t>(), ctl, g->m / 32,
-                                                  w.rowflag.as<uint8_t>(), reinterpret_cast<int*>(ctl + 1));
+            MarkArgs MA{mm->nz_in, words, g->out_off.as<uint64_t>(), g->out_tgt.as<uint32_t>(), ctl,
+                        g->m / g->sparse_div, w.rowflag.as<uint8_t>(), reinterpret_cast<int*>(ctl + 1),
+                        w.wbits.as<uint32_t>(), by_win ? w.wl.as<uint32_t>() : nullptr, wl_cnt, rb_shift,
+                        w.big.as<ulonglong2>(), wl_cnt + 1};
+            k_mark_out<<<gb, 256, 0, g->stream>>>(MA);
             CKL("k_mark_out");
-            g->launches += 2;
+            k_mark_big<<<4 * g->num_sms, 256, 0, g->stream>>>(MA);
+            if (by_win) {
+                CKL("k_mark_big");
+                const LongRows& L = g->longs;
+                k_long_list<<<grid_for(std::max<uint32_t>(L.n_long, 1), 256, 4 * g->num_sms), 256, 0, g->stream>>>(
+                    MA, L.seg_row.as<uint32_t>(), L.long_first.as<uint32_t>(), L.long_nseg.as<uint32_t>(),
+                    L.n_long, w.sl.as<uint32_t>(), wl_cnt + 2);
+                g->launches += 1;
+            }
+            CKL("k_mark_big");
+            g->launches += 3;
             P.rowflag = w.rowflag.as<uint8_t>();
             P.dense = reinterpret_cast<const int*>(ctl + 1);
+            if (by_win) {
+                P.wl = w.wl.as<uint32_t>();
+                P.wl_cnt = wl_cnt;
+                P.win_blk = g->longs.win_blk_w[LongRows::wi(rb)].as<uint32_t>();
+                P.sl = w.sl.as<uint32_t>();
+                P.sl_cnt = wl_cnt + 2;
+            }
         }
         if (spmm_version(B) == 5) {
             const bool last = a.out != nullptr;
@@ -710,7 +753,21 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         g->launches += 1;  // + the epilogue below
     } else switch (B) {
         case 1:
-            if (spmv_version() == 2)
+            if (spmv_version() == 3) {
+                static const int grid3 = [] {
+                    int occ = 0, dev = 0, sms = 0;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmv3, kMv3Threads, 0));
+                    CK(cudaGetDevice(&dev));
+                    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                    return std::max(occ, 1) * sms;
+                }();
+                const LongRows& L = g->longs;
+                Mv3Args M{a, L.seg_row.as<uint32_t>(), L.seg_lo.as<int64_t>(), L.seg_long.as<uint32_t>(),
+                          L.long_first.as<uint32_t>(), L.long_nseg.as<uint32_t>(), L.n_segs,
+                          L.blocks_w[3].as<uint2>(), L.n_blocks_w[3], w.long_cnt.as<uint32_t>(),
+                          w.seg_part.as<double>(), w.fx.as<unsigned long long>()};
+                k_step_spmv3<<<grid3, kMv3Threads, 0, g->stream>>>(M);
+            } else if (spmv_version() == 2)
                 k_step_spmv2<<<grid, block, 0, g->stream>>>(MvArgs{a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>()});
             else
                 k_step_spmv<<<grid, block, 0, g->stream>>>(a);
@@ -1096,9 +1153,12 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
             put(L.long_nseg, long_nseg.data(), long_nseg.size() * 4);
             // short-row blocks: consecutive short rows inside one aligned
             // window, at most kBlockNnz nnz (a lone row may reach kLong)
+            std::vector<uint32_t> win_first;
             auto make_blocks = [&](uint32_t win) {
                 std::vector<uint2> blocks;
+                win_first.clear();
                 for (uint32_t w0 = 0; w0 < n; w0 += win) {
+                    win_first.push_back((uint32_t)blocks.size());
                     const uint32_t w1 = std::min<uint32_t>(n, w0 + win);
                     uint32_t r = w0;
                     while (r < w1) {
@@ -1117,13 +1177,15 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
                         blocks.push_back(make_uint2(b0, r - b0));
                     }
                 }
+                win_first.push_back((uint32_t)blocks.size());
                 return blocks;
             };
             std::vector<uint2> blocks = make_blocks(kMmRows);
             put(L.blocks, blocks.data(), blocks.size() * sizeof(uint2));
-            for (int rows : {4, 8, 16}) {
+            for (int rows : {4, 8, 16, 32}) {
                 std::vector<uint2> bw = make_blocks(rows);
                 put(L.blocks_w[LongRows::wi(rows)], bw.data(), bw.size() * sizeof(uint2));
+                put(L.win_blk_w[LongRows::wi(rows)], win_first.data(), win_first.size() * 4);
                 L.n_blocks_w[LongRows::wi(rows)] = (uint32_t)bw.size();
             }
             g->n_blocks = (uint32_t)blocks.size();
@@ -1165,7 +1227,9 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->mv.item_nnz.release();
             for (DevBuf* d : {&g->longs.seg_row, &g->longs.seg_lo, &g->longs.seg_long, &g->longs.long_first,
                               &g->longs.long_nseg, &g->longs.blocks, &g->longs.blocks_w[0],
-                              &g->longs.blocks_w[1], &g->longs.blocks_w[2]})
+                              &g->longs.blocks_w[1], &g->longs.blocks_w[2], &g->longs.blocks_w[3],
+                              &g->longs.win_blk_w[0], &g->longs.win_blk_w[1], &g->longs.win_blk_w[2],
+                              &g->longs.win_blk_w[3]})
                 d->release();
             g->init_part.release();
             g->out_stage.release();
