@@ -153,6 +153,50 @@ int tpa_query_batch(tpa_graph *g, const tpa_artifact *a, const uint32_t *seeds, 
 int tpa_query_na_batch(tpa_graph *g, const uint32_t *seeds, uint32_t B, uint32_t S, uint32_t T,
                        double c, double eps, double *out, int flags);
 
+/* --- multi-GPU: row-partitioned CPI (B = 1) ---------------------------------
+ * The north star's multi-GPU layout: the rows of CSR(Ãᵀ) are split into
+ * nnz-balanced ranges, one per GPU; each sweep is the single-GPU kernel on
+ * the partition's rows followed by an all-reduce of the exact fixed-point
+ * residual / dangling totals and an in-place all-gather of the iterate's
+ * shares.  Results equal the whole-graph run bit for bit (the totals are
+ * exact integers and the per-row arithmetic is unchanged).
+ * Replaces, per rank: cpi_run / pagerank (cpi.hpp:49-57) and preprocess's
+ * stranger vector (tpa.hpp:27-28); queries run on whole-graph replicas
+ * (tpa_graph_create) since each seed is independent. */
+#define TPA_COMM_ID_BYTES 128
+
+/* A fresh NCCL unique id (rank 0 creates it and sends it to the others). */
+int tpa_comm_unique_id(void *id_out /* TPA_COMM_ID_BYTES */);
+
+/* One process per GPU: partition `rank` of `nranks`; collective over the
+ * ranks (NCCL communicator built from comm_id).  nranks = 1 needs no id.
+ * tpa_cpi_run and tpa_preprocess (no artifact) on this handle are collective
+ * calls: every rank passes the same arguments and receives the full n-vector;
+ * the other compute entry points refuse a partition.  tpa_graph_info reports
+ * the graph's n and m. */
+int tpa_graph_create_part(uint32_t n, uint64_t m, const uint64_t *out_offsets,
+                          const uint32_t *out_targets, int policy, uint64_t fingerprint, int device,
+                          uint32_t nranks, uint32_t rank, const void *comm_id, tpa_graph **out);
+/* Partition geometry: rows [row_begin, row_end) of `nranks`; `slice` = padded
+ * rows per partition in the share layout. */
+int tpa_graph_part_info(const tpa_graph *g, uint32_t *nranks, uint32_t *rank, uint32_t *row_begin,
+                        uint32_t *row_end, uint32_t *slice);
+
+/* One process driving `nparts` partitions on devices[0..nparts) (a device may
+ * repeat); exchanges by stream-ordered peer copies, no NCCL. */
+typedef struct tpa_group tpa_group;
+int tpa_group_create(uint32_t n, uint64_t m, const uint64_t *out_offsets, const uint32_t *out_targets,
+                     int policy, uint64_t fingerprint, const int *devices, uint32_t nparts,
+                     tpa_group **out);
+int tpa_group_destroy(tpa_group *grp);
+int tpa_group_part(tpa_group *grp, uint32_t r, tpa_graph **out); /* borrowed; info calls only */
+/* cpi_run semantics (as tpa_cpi_run); out_scores: n doubles, host or device (UVA). */
+int tpa_group_cpi_run(tpa_group *grp, const uint32_t *seeds, uint64_t n_seeds, double c, double eps,
+                      uint32_t start_iter, int64_t terminal_iter, double *out_scores,
+                      uint32_t *iterations_run, int *converged, double *residual_l1);
+/* preprocess's stranger vector (window [T, inf)); out: n doubles. */
+int tpa_group_preprocess(tpa_group *grp, double c, double eps, uint32_t T, double *out_stranger);
+
 /* --- host-side graph plumbing (not on the hot path) -----------------------
  * A host graph with the reference Graph's construction semantics
  * (graph.cpp:53-91: sort, dedupe, pre-policy dangling list, SelfLoop repair,

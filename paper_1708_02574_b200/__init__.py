@@ -7,6 +7,7 @@ include/tpa_gpu.h.  No CPU fallback: importing fails if the library is absent.
 from ._native import CudaError
 from .graph import (DanglingPolicy, DeviceGraph, Graph, dangling_policy_from_string, fingerprint,
                     generate_random_graph, generate_rmat, propagation_sweep, sample_seeds, to_string)
+from .partition import PartitionedGraph, PartitionGroup, partition_rows
 from .tpa import (CpiParams, CpiResult, SeedSet, StrangerArtifact, TpaParams, cpi_partition, cpi_run,
                   exact_rwr, exact_rwr_batch, kDefaultRestartProb, kDefaultTolerance, neighbor_scale_factor,
                   pagerank, preprocess, query, query_batch, query_na)
@@ -17,4 +18,5 @@ __all__ = [
     "CpiParams", "CpiResult", "SeedSet", "StrangerArtifact", "TpaParams", "cpi_partition", "cpi_run",
     "exact_rwr", "exact_rwr_batch", "kDefaultRestartProb", "kDefaultTolerance", "neighbor_scale_factor",
     "pagerank", "preprocess", "query", "query_batch", "query_na",
+    "PartitionedGraph", "PartitionGroup", "partition_rows",
 ]

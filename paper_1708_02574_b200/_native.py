@@ -51,6 +51,16 @@ SIGNATURES = {
     "tpa_query": ([_vp, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_query_batch": ([_vp, _vp, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_query_na_batch": ([_vp, _vp, _u32, _u32, _u32, _dbl, _dbl, _vp, _int], _int),
+    "tpa_comm_unique_id": ([_vp], _int),
+    "tpa_graph_create_part": ([_u32, _u64, _vp, _vp, _int, _u64, _int, _u32, _u32, _vp, C.POINTER(_vp)], _int),
+    "tpa_graph_part_info": ([_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32),
+                             C.POINTER(_u32)], _int),
+    "tpa_group_create": ([_u32, _u64, _vp, _vp, _int, _u64, _vp, _u32, C.POINTER(_vp)], _int),
+    "tpa_group_destroy": ([_vp], _int),
+    "tpa_group_part": ([_vp, _u32, C.POINTER(_vp)], _int),
+    "tpa_group_cpi_run": ([_vp, _vp, _u64, _dbl, _dbl, _u32, _i64, _vp, C.POINTER(_u32), C.POINTER(_int),
+                           C.POINTER(_dbl)], _int),
+    "tpa_group_preprocess": ([_vp, _dbl, _dbl, _u32, _vp], _int),
     "tpa_host_graph_from_edges": ([_u32, _vp, _vp, _u64, _int, C.POINTER(_vp)], _int),
     "tpa_host_graph_rmat": ([_u32, _u32, _dbl, _dbl, _dbl, _u64, _int, _int, C.POINTER(_vp)], _int),
     "tpa_host_graph_random": ([_u32, _u64, _u64, _int, C.POINTER(_vp)], _int),

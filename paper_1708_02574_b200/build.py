@@ -27,13 +27,18 @@ NVCC_FLAGS = [
 ]
 
 
+# NCCL (multi-GPU partitions) is opened at first use (tpa_part.cuh), not
+# linked: torch must keep its own libnccl.so.2 whatever the import order.
+LIBS = ["-ldl"]
+
+
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
 def deps():
     return sources() + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
-                              if f.endswith((".cuh", ".hpp", ".h"))) + [os.path.join(INCLUDE, "tpa_gpu.h")]
+                              if f.endswith((".cuh", ".hpp", ".h", ".inl"))) + [os.path.join(INCLUDE, "tpa_gpu.h")]
 
 
 def up_to_date() -> bool:
@@ -48,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     tmp = LIB + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-I", INCLUDE, "-I", CSRC, "-o", tmp, *sources()]
+    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-I", INCLUDE, "-I", CSRC, "-o", tmp, *sources(), *LIBS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:

@@ -6,9 +6,13 @@
 //   * the tile's nnz range travels with the work item, so the index loads,
 //     the row_ptr loads and the per-row out-degree / accumulator loads are all
 //     issued at once (one round trip), then the gathers (a second one);
-//   * the L1 residual and dangling mass are reduced per CTA in a fixed tree
-//     and added across CTAs as exact 128-bit fixed-point integers (order-free),
-//     replacing v1's two-level ticket tree; the last CTA advances the state.
+//   * every row's |y| (and dangling y) is added as an exact 128-bit
+//     fixed-point integer (order-free), per thread, then per CTA, then across
+//     CTAs: the totals do not depend on how rows are grouped into tiles, CTAs
+//     or GPU partitions, so a row-partitioned run (cpi_part.cuh) reproduces
+//     the one-GPU residuals bit for bit; the last CTA advances the state, or,
+//     for a partition, publishes its totals as carry-free limbs for an
+//     all-reduce (fx_to_limbs) and leaves the state to k_part_finalize.
 #pragma once
 
 #include "cpi_spmm.cuh"
@@ -19,7 +23,36 @@ struct MvArgs {
     StepArgs s;
     const longlong2* __restrict__ item_nnz;  // [n_items] {nnz begin, nnz end}
     unsigned long long* fx;                  // [4]: l1 hi/lo, dm hi/lo; zero between launches
+    unsigned long long* limbs;               // partition mode: [6] out (see fx_to_limbs), else null
 };
+
+// 128-bit fixed-point totals as three limbs each (hi, lo >> 32, lo & 2^32-1):
+// limb-wise integer sums over up to 2^31 partitions cannot overflow, and
+// limbs_to_fx restores the exact 128-bit total (NCCL all-reduce of uint64).
+__device__ __forceinline__ void fx_to_limbs(unsigned long long hi, unsigned long long lo, unsigned long long* L) {
+    L[0] = hi;
+    L[1] = lo >> 32;
+    L[2] = lo & 0xffffffffull;
+}
+__device__ __forceinline__ void limbs_to_fx(const unsigned long long* L, unsigned long long& hi,
+                                            unsigned long long& lo) {
+    const unsigned long long t2 = L[2];
+    const unsigned long long t1 = L[1] + (t2 >> 32);
+    lo = ((t1 & 0xffffffffull) << 32) | (t2 & 0xffffffffull);
+    hi = L[0] + (t1 >> 32);
+}
+
+// ColState after sweep `step` from the global residual / dangling mass
+// (cpi.cpp:73-80; Uniform spread graph.cpp:265-268).
+__device__ __forceinline__ ColState advance_state(ColState s, double res, double dmt, const StepArgs& a) {
+    s.residual = res;
+    s.iters = a.step;
+    s.converged = res < a.eps;
+    s.active = !s.converged && (a.terminal < 0 || (int64_t)a.step < a.terminal);
+    s.has_spread = (a.policy == kUniform && dmt != 0.0);
+    s.spread = s.has_spread ? ddiv(dmul(a.keep, dmt), (double)a.n) : 0.0;
+    return s;
+}
 
 __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     const StepArgs& a = M.s;
@@ -42,11 +75,15 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         // column stopped earlier: only a pending combine remains (tpa.cpp:73)
         if (a.out)
             for (uint32_t v = rb + tid; v < re; v += kThreads) combine_only(a, v, 0, 1, v);
-        if (item == 0 && tid == 0) a.state_out[0] = st;
+        if (item == 0 && tid == 0) {
+            a.state_out[0] = st;
+            if (M.limbs)
+                for (int k = 0; k < 6; ++k) M.limbs[k] = 0ull;
+        }
         return;
     }
     const bool want_dm = a.policy == kUniform;
-    double my_l1 = 0.0, my_dm = 0.0;
+    unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;  // this thread's exact |y| and dangling sums
 
     if (!is_long) {
         const uint32_t nrows = re - rb;
@@ -126,8 +163,8 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
                 }
             }
             if (a.share_out) a.share_out[vtx] = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
-            my_l1 = dadd(my_l1, fabs(y));
-            if (want_dm && dg[q] == 0) my_dm = dadd(my_dm, y);
+            fx_add(f0, f1, y);
+            if (want_dm && dg[q] == 0) fx_add(f2, f3, y);
         }
     } else {
         // one long row: every thread sums a fixed strided subset, then a fixed tree
@@ -149,43 +186,60 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
             const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
-            my_l1 = fabs(y);
-            if (want_dm && d == 0) my_dm = y;
+            fx_add(f0, f1, y);
+            if (want_dm && d == 0) fx_add(f2, f3, y);
         }
     }
-    // CTA partials (fixed tree) -> exact fixed-point totals across CTAs
-    const double l1 = block_sum(my_l1, s_red);
-    const double dm = want_dm ? block_sum(my_dm, s_red) : 0.0;
+    // exact integer totals: thread -> CTA (shared) -> grid
+    __shared__ unsigned long long s_fx[4];
+    if (tid < 4) s_fx[tid] = 0ull;
+    __syncthreads();
+    if (f0 | f1) fx_atomic_add(&s_fx[0], &s_fx[1], f0, f1);
+    if (f2 | f3) fx_atomic_add(&s_fx[2], &s_fx[3], f2, f3);
+    __syncthreads();
     if (tid == 0) {
-        unsigned long long h = 0, l = 0;
-        if (l1 != 0.0) {
-            fx_add(h, l, l1);
-            fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
-        }
-        if (dm != 0.0) {
-            h = l = 0;
-            fx_add(h, l, dm);
-            fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
-        }
+        if (s_fx[0] | s_fx[1]) fx_atomic_add(&M.fx[0], &M.fx[1], s_fx[0], s_fx[1]);
+        if (s_fx[2] | s_fx[3]) fx_atomic_add(&M.fx[2], &M.fx[3], s_fx[2], s_fx[3]);
         __threadfence();
         s_ticket = atomicAdd(a.done_cnt, 1u);
     }
     __syncthreads();
     if (s_ticket != gridDim.x - 1 || tid != 0) return;
     __threadfence();
-    // last CTA: cpi.cpp:73-80, then reset the accumulators
-    ColState s = st;
-    const double res = fx_decode(atomicAdd(&M.fx[0], 0ull), atomicAdd(&M.fx[1], 0ull));
-    const double dmt = fx_decode(atomicAdd(&M.fx[2], 0ull), atomicAdd(&M.fx[3], 0ull));
-    s.residual = res;
-    s.iters = a.step;
-    s.converged = res < a.eps;
-    s.active = !s.converged && (a.terminal < 0 || (int64_t)a.step < a.terminal);
-    s.has_spread = (a.policy == kUniform && dmt != 0.0);
-    s.spread = s.has_spread ? ddiv(dmul(a.keep, dmt), (double)a.n) : 0.0;
-    a.state_out[0] = s;
+    const unsigned long long h0 = atomicAdd(&M.fx[0], 0ull), l0 = atomicAdd(&M.fx[1], 0ull);
+    const unsigned long long h1 = atomicAdd(&M.fx[2], 0ull), l1 = atomicAdd(&M.fx[3], 0ull);
+    if (M.limbs) {
+        // a partition's totals: all-reduced, then k_part_finalize advances the state
+        fx_to_limbs(h0, l0, M.limbs);
+        fx_to_limbs(h1, l1, M.limbs + 3);
+    } else {
+        // last CTA: cpi.cpp:73-80
+        a.state_out[0] = advance_state(st, fx_decode(h0, l0), fx_decode(h1, l1), a);
+    }
     M.fx[0] = M.fx[1] = M.fx[2] = M.fx[3] = 0ull;
     *a.done_cnt = 0;
+}
+
+// Partition mode, after the all-reduce of every partition's limbs: the same
+// state on every GPU.  init: x⁽⁰⁾'s state (k_init_finish's role).
+__global__ void k_part_finalize(const unsigned long long* __restrict__ limbs, StepArgs a, int init, int active0) {
+    unsigned long long h0, l0, h1, l1;
+    limbs_to_fx(limbs, h0, l0);
+    limbs_to_fx(limbs + 3, h1, l1);
+    const double res = fx_decode(h0, l0), dmt = fx_decode(h1, l1);
+    if (init) {
+        ColState s;
+        s.residual = res;
+        s.iters = 0;
+        s.active = active0;
+        s.converged = 0;
+        s.has_spread = a.policy == kUniform && dmt != 0.0;
+        s.spread = s.has_spread ? ddiv(dmul(a.keep, dmt), (double)a.n) : 0.0;
+        a.state_out[0] = s;
+        return;
+    }
+    const ColState st = a.state_in[0];
+    a.state_out[0] = st.active ? advance_state(st, res, dmt, a) : st;
 }
 
 }  // namespace tpa

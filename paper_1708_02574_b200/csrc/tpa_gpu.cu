@@ -9,6 +9,7 @@
 // Per-width workspace (B = 1, 8, 16, 32, 64): share ping-pong [n][B] fp64,
 // acc [n][B] fp64, reduction partials, ticket counters, ColState x2.
 #include <cub/device/device_radix_sort.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -143,46 +144,52 @@ __global__ void k_row_ptr(const uint32_t* __restrict__ keys, uint64_t m, uint32_
 // ---------------------------------------------------------------------------
 // Dense B = 1 start: PageRank (x == null: every node gets `weight`,
 // SeedSet::all_nodes) or an explicit x (propagation_sweep / multi-seed sets).
+// |x⁰| and the dangling mass go into exact fixed-point totals (fx[4], zero on
+// entry) like the sweeps', so a row partition sees the same x⁰ state.
 __global__ void __launch_bounds__(kThreads)
 k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
              const uint32_t* __restrict__ deg, double keep, double* __restrict__ share0,
-             double* __restrict__ acc0, double* __restrict__ part) {
-    __shared__ double s_red[kThreads];
-    double l1 = 0.0, dm = 0.0;
-    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
-    const uint64_t lo = blockIdx.x * per, hi = min((uint64_t)n, lo + per);
-    for (uint64_t u = lo + threadIdx.x; u < hi; u += kThreads) {
+             double* __restrict__ acc0, unsigned long long* fx) {
+    __shared__ unsigned long long s_fx[4];
+    if (threadIdx.x < 4) s_fx[threadIdx.x] = 0ull;
+    __syncthreads();
+    unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+    for (uint64_t u = blockIdx.x * (uint64_t)kThreads + threadIdx.x; u < n; u += (uint64_t)gridDim.x * kThreads) {
         const double xv = x ? x[u] : weight;
         const uint32_t d = deg[u];
         share0[u] = d ? ddiv(dmul(keep, xv), (double)d) : 0.0;
         if (acc0) acc0[u] = xv;
-        l1 = dadd(l1, fabs(xv));
-        if (d == 0) dm = dadd(dm, xv);
+        fx_add(f0, f1, xv);
+        if (d == 0) fx_add(f2, f3, xv);
     }
-    l1 = block_sum(l1, s_red);
-    dm = block_sum(dm, s_red);
+    if (f0 | f1) fx_atomic_add(&s_fx[0], &s_fx[1], f0, f1);
+    if (f2 | f3) fx_atomic_add(&s_fx[2], &s_fx[3], f2, f3);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = l1;
-        part[2 * blockIdx.x + 1] = dm;
+        if (s_fx[0] | s_fx[1]) fx_atomic_add(&fx[0], &fx[1], s_fx[0], s_fx[1]);
+        if (s_fx[2] | s_fx[3]) fx_atomic_add(&fx[2], &fx[3], s_fx[2], s_fx[3]);
     }
 }
 
-__global__ void __launch_bounds__(kThreads)
-k_init_finish(const double* __restrict__ part, uint32_t nblocks, int policy, double keep,
-              uint32_t n, int active0, ColState* state0) {
-    __shared__ double s_scr[kThreads];
-    __shared__ double s_fin[2];
-    ordered_column_sums(part, nblocks, 2, s_scr, s_fin);
-    if (threadIdx.x == 0) {
+// x⁰'s ColState from the totals (then fx is zeroed for the sweeps); a
+// partition instead publishes limbs for the all-reduce + k_part_finalize.
+__global__ void k_init_finish(unsigned long long* fx, unsigned long long* limbs, int policy, double keep,
+                              uint32_t n, int active0, ColState* state0) {
+    if (limbs) {
+        fx_to_limbs(fx[0], fx[1], limbs);
+        fx_to_limbs(fx[2], fx[3], limbs + 3);
+    } else {
+        const double l1 = fx_decode(fx[0], fx[1]), dm = fx_decode(fx[2], fx[3]);
         ColState s;
-        s.residual = s_fin[0];
+        s.residual = l1;
         s.iters = 0;
         s.active = active0;
         s.converged = 0;
-        s.has_spread = policy == kUniform && s_fin[1] != 0.0;
-        s.spread = s.has_spread ? ddiv(dmul(keep, s_fin[1]), (double)n) : 0.0;
+        s.has_spread = policy == kUniform && dm != 0.0;
+        s.spread = s.has_spread ? ddiv(dmul(keep, dm), (double)n) : 0.0;
         state0[0] = s;
     }
+    fx[0] = fx[1] = fx[2] = fx[3] = 0ull;
 }
 
 // Up to 64 seeds travel as a kernel parameter: no host->device copy, so
@@ -440,6 +447,7 @@ struct Workspace {
     DevBuf rowflag, sparse_ctl;  // sparse sweeps: reachable rows; {cost, dense, window count}
     DevBuf wbits, wl;            // sparse sweeps: marked windows (bitmap, list)
     DevBuf big;                  // sparse sweeps: edge chunks of high out-degree frontier rows
+    DevBuf limbs;                // partition mode: [3][6] fixed-point limbs (sweep parity 0/1, init) + [6] totals
     DevBuf sl;                   // sparse sweeps: segments of the marked long rows
     int grid_gather = 0, grid_epi = 0;
 };
@@ -454,6 +462,23 @@ struct LongRows {
     uint32_t n_blocks_w[4] = {0, 0, 0, 0};
     DevBuf win_blk_w[4];  // per window: index of its first block (n_windows + 1 entries)
     static int wi(int rows) { return rows == 4 ? 0 : rows == 8 ? 1 : rows == 16 ? 2 : 3; }
+};
+
+// A row partition of CSR(Ãᵀ) for multi-GPU CPI (the north star's layout):
+// partition r owns rows [bounds[r], bounds[r+1]) (balanced by nnz) and their
+// y / acc; the iterate's shares live in a padded global layout of
+// nranks x slice doubles (row v of partition r at r*slice + v - bounds[r]),
+// so one in-place all-gather per sweep assembles the full share vector and
+// the column indices are stored pre-mapped to that layout.
+struct PartInfo {
+    uint32_t nranks = 1, rank = 0;
+    uint32_t n_global = 0;
+    uint64_t m_global = 0;
+    std::vector<uint32_t> bounds;  // nranks + 1
+    uint32_t slice = 0;
+    ncclComm_t comm = nullptr;     // one rank per process; null: in-process group or nranks = 1
+    uint32_t row_begin() const { return bounds[rank]; }
+    uint32_t rows(uint32_t r) const { return bounds[r + 1] - bounds[r]; }
 };
 
 }  // namespace tpa
@@ -477,6 +502,7 @@ struct tpa_graph {
     DevBuf init_part;
     DevBuf out_stage;  // host-output staging for batch calls
     std::set<tpa_artifact*> artifacts;  // detached (buffers freed) on destroy
+    std::unique_ptr<PartInfo> part;     // row partition (multi-GPU), or null: whole graph
     uint64_t launches = 0;
     int num_sms = 148;
     std::mutex mu;
@@ -518,7 +544,9 @@ struct tpa_graph {
         const uint32_t items = B == 1 ? mv.n_items : 1, groups = B == 1 ? mv.n_groups : 1;
         // B > 1: one extra all-zero row (index n) that dead sources gather
         const size_t nb = (size_t)n * B * sizeof(double);
-        const size_t nbs = nb + (B > 1 ? (size_t)B * sizeof(double) : 0);
+        // a partition's shares span the padded global layout (all partitions)
+        const size_t nbs = part ? (size_t)part->nranks * part->slice * sizeof(double)
+                                : nb + (B > 1 ? (size_t)B * sizeof(double) : 0);
         if (w.share[0].bytes < nbs) {
             w.share[0].ensure(nbs, stream);
             w.share[1].ensure(nbs, stream);
@@ -753,7 +781,7 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         g->launches += 1;  // + the epilogue below
     } else switch (B) {
         case 1:
-            if (spmv_version() == 3) {
+            if (spmv_version() == 3 && !g->part) {
                 static const int grid3 = [] {
                     int occ = 0, dev = 0, sms = 0;
                     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmv3, kMv3Threads, 0));
@@ -767,8 +795,18 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                           L.blocks_w[3].as<uint2>(), L.n_blocks_w[3], w.long_cnt.as<uint32_t>(),
                           w.seg_part.as<double>(), w.fx.as<unsigned long long>()};
                 k_step_spmv3<<<grid3, kMv3Threads, 0, g->stream>>>(M);
-            } else if (spmv_version() == 2)
-                k_step_spmv2<<<grid, block, 0, g->stream>>>(MvArgs{a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>()});
+            } else if (spmv_version() == 2 || g->part)
+            {
+                static const bool carve = [] {  // A/B: shared-memory carveout (L1 share) for v2
+                    const char* e = std::getenv("TPA_MV_CARVEOUT");
+                    if (e) CK(cudaFuncSetAttribute(k_step_spmv2, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
+                    return e != nullptr;
+                }();
+                (void)carve;
+                k_step_spmv2<<<grid, block, 0, g->stream>>>(MvArgs{
+                    a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
+                    g->part ? w.limbs.as<unsigned long long>() + (a.step & 1) * 6 : nullptr});
+            }
             else
                 k_step_spmv<<<grid, block, 0, g->stream>>>(a);
             break;
@@ -833,13 +871,12 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int active0 = cfg.terminal != 0;
     if (cfg.init == Init::Dense) {
         const int nblk = grid_for(n, 4 * kThreads, 4 * g->num_sms);
-        g->init_part.ensure((size_t)nblk * 2 * sizeof(double), g->stream);
         k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.d_x, cfg.weight, n, g->deg.as<uint32_t>(), keep,
                                                        w.share[0].as<double>(), acc0,
-                                                       g->init_part.as<double>());
+                                                       w.fx.as<unsigned long long>());
         CKL("k_init_dense");
-        k_init_finish<<<1, kThreads, 0, g->stream>>>(g->init_part.as<double>(), nblk, g->policy, keep, n,
-                                                     active0, st);
+        k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), nullptr, g->policy, keep, n,
+                                              active0, st);
         CKL("k_init_finish");
         g->launches += 2;
     } else if (mm) {
@@ -1040,6 +1077,112 @@ static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, d
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+namespace tpa {
+static void require_whole(const tpa_graph* g, const char* what);
+static void part_comm_destroy(ncclComm_t c);
+static void part_cpi_run(std::vector<tpa_graph*>& Pg, const uint32_t* seeds, uint64_t n_seeds, double c,
+                         double eps, uint32_t start_iter, int64_t terminal_iter, double* out_scores,
+                         uint32_t* iterations_run, int* converged, double* residual_l1);
+static void part_preprocess(std::vector<tpa_graph*>& Pg, double c, double eps, uint32_t T, double* out);
+static void require_solo_part(const tpa_graph* g) {
+    if (g->part->nranks > 1 && !g->part->comm)
+        throw std::invalid_argument("a group partition runs through the tpa_group_* calls");
+}
+}  // namespace tpa
+
+// Work schedules over the rows of CSR(Ãᵀ) (row_ptr rp, n rows): SpMV tiles,
+// SpMM long-row segments and short-row blocks.
+static void build_schedules(tpa_graph* g, const std::vector<int64_t>& rp, uint32_t n) {
+    cudaStream_t s = g->stream;
+    auto mv = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
+    if (mv.size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
+    {
+        // SpMM long rows: kLong-nnz segments, longest rows first
+        std::vector<std::pair<int64_t, uint32_t>> lr;
+        for (uint32_t v = 0; v < n; ++v)
+            if (rp[v + 1] - rp[v] > kLong) lr.push_back({rp[v + 1] - rp[v], v});
+        std::stable_sort(lr.begin(), lr.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+        std::vector<uint32_t> seg_row, seg_long, long_first, long_nseg;
+        std::vector<int64_t> seg_lo;
+        for (uint32_t li = 0; li < lr.size(); ++li) {
+            const uint32_t v = lr[li].second;
+            const uint32_t ns = (uint32_t)((lr[li].first + kLong - 1) / kLong);
+            long_first.push_back((uint32_t)seg_row.size());
+            long_nseg.push_back(ns);
+            for (uint32_t k = 0; k < ns; ++k) {
+                seg_row.push_back(v);
+                seg_lo.push_back(rp[v] + (int64_t)k * kLong);
+                seg_long.push_back(li);
+            }
+        }
+        LongRows& L = g->longs;
+        L.n_long = (uint32_t)lr.size();
+        L.n_segs = (uint32_t)seg_row.size();
+        auto put = [&](DevBuf& d, const void* src, size_t bytes) {
+            d.ensure(std::max<size_t>(bytes, 16), g->stream);
+            if (bytes) CK(cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, s));
+        };
+        put(L.seg_row, seg_row.data(), seg_row.size() * 4);
+        put(L.seg_lo, seg_lo.data(), seg_lo.size() * 8);
+        put(L.seg_long, seg_long.data(), seg_long.size() * 4);
+        put(L.long_first, long_first.data(), long_first.size() * 4);
+        put(L.long_nseg, long_nseg.data(), long_nseg.size() * 4);
+        // short-row blocks: consecutive short rows inside one aligned
+        // window, at most kBlockNnz nnz (a lone row may reach kLong)
+        std::vector<uint32_t> win_first;
+        auto make_blocks = [&](uint32_t win) {
+            std::vector<uint2> blocks;
+            win_first.clear();
+            for (uint32_t w0 = 0; w0 < n; w0 += win) {
+                win_first.push_back((uint32_t)blocks.size());
+                const uint32_t w1 = std::min<uint32_t>(n, w0 + win);
+                uint32_t r = w0;
+                while (r < w1) {
+                    if (rp[r + 1] - rp[r] > kLong) {
+                        ++r;
+                        continue;
+                    }
+                    const uint32_t b0 = r;
+                    int64_t nnz = 0;
+                    while (r < w1 && rp[r + 1] - rp[r] <= kLong) {
+                        const int64_t L2 = rp[r + 1] - rp[r];
+                        if (r > b0 && nnz + L2 > kBlockNnz) break;
+                        nnz += L2;
+                        ++r;
+                    }
+                    blocks.push_back(make_uint2(b0, r - b0));
+                }
+            }
+            win_first.push_back((uint32_t)blocks.size());
+            return blocks;
+        };
+        std::vector<uint2> blocks = make_blocks(kMmRows);
+        put(L.blocks, blocks.data(), blocks.size() * sizeof(uint2));
+        for (int rows : {4, 8, 16, 32}) {
+            std::vector<uint2> bw = make_blocks(rows);
+            put(L.blocks_w[LongRows::wi(rows)], bw.data(), bw.size() * sizeof(uint2));
+            put(L.win_blk_w[LongRows::wi(rows)], win_first.data(), win_first.size() * 4);
+            L.n_blocks_w[LongRows::wi(rows)] = (uint32_t)bw.size();
+        }
+        g->n_blocks = (uint32_t)blocks.size();
+        CK(cudaStreamSynchronize(s));
+    }
+    g->mv.n_items = (uint32_t)mv.size();
+    g->mv.n_groups = (g->mv.n_items + kGroupItems - 1) / kGroupItems;
+    g->mv.items.ensure(mv.size() * sizeof(uint2), g->stream);
+    CK(cudaMemcpyAsync(g->mv.items.p, mv.data(), mv.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    {
+        std::vector<longlong2> nr(mv.size());
+        for (size_t i = 0; i < mv.size(); ++i) {
+            const uint32_t rb = mv[i].x, re = mv[i].y & ~kLongFlag;
+            nr[i] = make_longlong2(rp[rb], rp[re]);
+        }
+        g->mv.item_nnz.ensure(nr.size() * sizeof(longlong2), g->stream);
+        CK(cudaMemcpyAsync(g->mv.item_nnz.p, nr.data(), nr.size() * sizeof(longlong2), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+}
+
 extern "C" {
 
 int tpa_abi_version(void) { return TPA_ABI_VERSION; }
@@ -1118,93 +1261,7 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         CK(cudaStreamSynchronize(s));
         g->launches += 4;
 
-        auto mv = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
-        if (mv.size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
-        {
-            // SpMM long rows: kLong-nnz segments, longest rows first
-            std::vector<std::pair<int64_t, uint32_t>> lr;
-            for (uint32_t v = 0; v < n; ++v)
-                if (rp[v + 1] - rp[v] > kLong) lr.push_back({rp[v + 1] - rp[v], v});
-            std::stable_sort(lr.begin(), lr.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-            std::vector<uint32_t> seg_row, seg_long, long_first, long_nseg;
-            std::vector<int64_t> seg_lo;
-            for (uint32_t li = 0; li < lr.size(); ++li) {
-                const uint32_t v = lr[li].second;
-                const uint32_t ns = (uint32_t)((lr[li].first + kLong - 1) / kLong);
-                long_first.push_back((uint32_t)seg_row.size());
-                long_nseg.push_back(ns);
-                for (uint32_t k = 0; k < ns; ++k) {
-                    seg_row.push_back(v);
-                    seg_lo.push_back(rp[v] + (int64_t)k * kLong);
-                    seg_long.push_back(li);
-                }
-            }
-            LongRows& L = g->longs;
-            L.n_long = (uint32_t)lr.size();
-            L.n_segs = (uint32_t)seg_row.size();
-            auto put = [&](DevBuf& d, const void* src, size_t bytes) {
-                d.ensure(std::max<size_t>(bytes, 16), g->stream);
-                if (bytes) CK(cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, s));
-            };
-            put(L.seg_row, seg_row.data(), seg_row.size() * 4);
-            put(L.seg_lo, seg_lo.data(), seg_lo.size() * 8);
-            put(L.seg_long, seg_long.data(), seg_long.size() * 4);
-            put(L.long_first, long_first.data(), long_first.size() * 4);
-            put(L.long_nseg, long_nseg.data(), long_nseg.size() * 4);
-            // short-row blocks: consecutive short rows inside one aligned
-            // window, at most kBlockNnz nnz (a lone row may reach kLong)
-            std::vector<uint32_t> win_first;
-            auto make_blocks = [&](uint32_t win) {
-                std::vector<uint2> blocks;
-                win_first.clear();
-                for (uint32_t w0 = 0; w0 < n; w0 += win) {
-                    win_first.push_back((uint32_t)blocks.size());
-                    const uint32_t w1 = std::min<uint32_t>(n, w0 + win);
-                    uint32_t r = w0;
-                    while (r < w1) {
-                        if (rp[r + 1] - rp[r] > kLong) {
-                            ++r;
-                            continue;
-                        }
-                        const uint32_t b0 = r;
-                        int64_t nnz = 0;
-                        while (r < w1 && rp[r + 1] - rp[r] <= kLong) {
-                            const int64_t L2 = rp[r + 1] - rp[r];
-                            if (r > b0 && nnz + L2 > kBlockNnz) break;
-                            nnz += L2;
-                            ++r;
-                        }
-                        blocks.push_back(make_uint2(b0, r - b0));
-                    }
-                }
-                win_first.push_back((uint32_t)blocks.size());
-                return blocks;
-            };
-            std::vector<uint2> blocks = make_blocks(kMmRows);
-            put(L.blocks, blocks.data(), blocks.size() * sizeof(uint2));
-            for (int rows : {4, 8, 16, 32}) {
-                std::vector<uint2> bw = make_blocks(rows);
-                put(L.blocks_w[LongRows::wi(rows)], bw.data(), bw.size() * sizeof(uint2));
-                put(L.win_blk_w[LongRows::wi(rows)], win_first.data(), win_first.size() * 4);
-                L.n_blocks_w[LongRows::wi(rows)] = (uint32_t)bw.size();
-            }
-            g->n_blocks = (uint32_t)blocks.size();
-            CK(cudaStreamSynchronize(s));
-        }
-        g->mv.n_items = (uint32_t)mv.size();
-        g->mv.n_groups = (g->mv.n_items + kGroupItems - 1) / kGroupItems;
-        g->mv.items.ensure(mv.size() * sizeof(uint2), g->stream);
-        CK(cudaMemcpyAsync(g->mv.items.p, mv.data(), mv.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
-        {
-            std::vector<longlong2> nr(mv.size());
-            for (size_t i = 0; i < mv.size(); ++i) {
-                const uint32_t rb = mv[i].x, re = mv[i].y & ~kLongFlag;
-                nr[i] = make_longlong2(rp[rb], rp[re]);
-            }
-            g->mv.item_nnz.ensure(nr.size() * sizeof(longlong2), g->stream);
-            CK(cudaMemcpyAsync(g->mv.item_nnz.p, nr.data(), nr.size() * sizeof(longlong2), cudaMemcpyHostToDevice, s));
-            CK(cudaStreamSynchronize(s));
-        }
+        build_schedules(g.get(), rp, n);
         CK(cudaStreamSynchronize(s));
         *out = g.release();
     });
@@ -1242,6 +1299,7 @@ int tpa_graph_destroy(tpa_graph* g) {
             }
             for (auto e : g->event_pool) cudaEventDestroy(e);
             if (g->own_stream) cudaStreamDestroy(g->stream);
+            if (g->part) part_comm_destroy(g->part->comm);
         }
         delete g;
     });
@@ -1266,8 +1324,8 @@ int tpa_graph_set_stream(tpa_graph* g, void* cuda_stream) {
 int tpa_graph_info(const tpa_graph* g, uint32_t* n, uint64_t* m, uint64_t* fingerprint, int* policy,
                    uint64_t* device_bytes) {
     return guard([&] {
-        if (n) *n = g->n;
-        if (m) *m = g->m;
+        if (n) *n = g->part ? g->part->n_global : g->n;  // the graph's size, also for a partition
+        if (m) *m = g->part ? g->part->m_global : g->m;
         if (fingerprint) *fingerprint = g->fingerprint;
         if (policy) *policy = g->policy;
         if (device_bytes) {
@@ -1320,6 +1378,7 @@ int tpa_graph_profile_read(tpa_graph* g, int width, int step, uint64_t* launches
 
 int tpa_graph_transpose(const tpa_graph* g, int64_t* row_ptr, uint32_t* col) {
     return guard([&] {
+        require_whole(g, "tpa_graph_transpose");
         DeviceGuard dg(g->device);
         if (row_ptr) CK(cudaMemcpy(row_ptr, g->row_ptr.p, (g->n + 1ull) * 8, cudaMemcpyDeviceToHost));
         if (col && g->m) CK(cudaMemcpy(col, g->col.p, g->m * 4, cudaMemcpyDeviceToHost));
@@ -1328,6 +1387,7 @@ int tpa_graph_transpose(const tpa_graph* g, int64_t* row_ptr, uint32_t* col) {
 
 int tpa_propagation_sweep(tpa_graph* g, const double* x, double* y, double c, int flags) {
     return guard([&] {
+        require_whole(g, "tpa_propagation_sweep");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         // graph.cpp:233-235
@@ -1366,6 +1426,13 @@ int tpa_cpi_run(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, double c,
     return guard([&] {
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
+        if (g->part) {  // collective over the partitions (cpi.cpp:87-101 per rank)
+            require_solo_part(g);
+            std::vector<tpa_graph*> Pg{g};
+            part_cpi_run(Pg, seeds, n_seeds, c, eps, start_iter, terminal_iter, out_scores, iterations_run,
+                         converged, residual_l1);
+            return;
+        }
         const bool dev = flags & TPA_DEVICE_PTRS;
         std::vector<uint32_t> hs;
         if (seeds) {
@@ -1417,6 +1484,7 @@ int tpa_cpi_run(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, double c,
 int tpa_cpi_partition(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, double c, double eps,
                       const uint32_t* boundaries, uint64_t n_boundaries, double* out, int flags) {
     return guard([&] {
+        require_whole(g, "tpa_cpi_partition");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         const bool dev = flags & TPA_DEVICE_PTRS;
@@ -1473,6 +1541,7 @@ int tpa_cpi_partition(tpa_graph* g, const uint32_t* seeds, uint64_t n_seeds, dou
 int tpa_exact_rwr_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, double c, double eps,
                         double* out, int flags) {
     return guard([&] {
+        require_whole(g, "tpa_exact_rwr_batch");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         if (B == 0) throw std::invalid_argument("seed set must not be empty");
@@ -1494,6 +1563,13 @@ int tpa_preprocess(tpa_graph* g, double c, double eps, uint32_t T, double* out_s
     return guard([&] {
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
+        if (g->part) {  // collective over the partitions; no device artifact (queries run on replicas)
+            require_solo_part(g);
+            if (out_artifact) throw std::invalid_argument("a row-partitioned graph returns the stranger vector only");
+            std::vector<tpa_graph*> Pg{g};
+            part_preprocess(Pg, c, eps, T, out_stranger);
+            return;
+        }
         if (T < 1) throw std::invalid_argument("stranger_start (T) must be at least 1");  // tpa.cpp:21-22
         validate_cpi(c, eps, T, -1);
         const bool dev = flags & TPA_DEVICE_PTRS;
@@ -1533,6 +1609,7 @@ int tpa_preprocess(tpa_graph* g, double c, double eps, uint32_t T, double* out_s
 int tpa_artifact_create(tpa_graph* g, const double* stranger, uint64_t graph_fingerprint, double c,
                         double eps, uint32_t T, int flags, tpa_artifact** out) {
     return guard([&] {
+        require_whole(g, "tpa_artifact_create");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         auto art = std::make_unique<tpa_artifact>();
@@ -1577,6 +1654,7 @@ static void check_query(tpa_graph* g, const tpa_artifact* a, uint32_t S) {
 
 int tpa_query(tpa_graph* g, const tpa_artifact* a, uint32_t seed, uint32_t S, double* out, int flags) {
     return guard([&] {
+        require_whole(g, "tpa_query");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         if (!a) throw std::invalid_argument("null artifact");
@@ -1590,6 +1668,7 @@ int tpa_query(tpa_graph* g, const tpa_artifact* a, uint32_t seed, uint32_t S, do
 int tpa_query_batch(tpa_graph* g, const tpa_artifact* a, const uint32_t* seeds, uint32_t B, uint32_t S,
                     double* out, int flags) {
     return guard([&] {
+        require_whole(g, "tpa_query_batch");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         if (!a) throw std::invalid_argument("null artifact");
@@ -1605,6 +1684,7 @@ int tpa_query_batch(tpa_graph* g, const tpa_artifact* a, const uint32_t* seeds, 
 int tpa_query_na_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, uint32_t S, uint32_t T, double c,
                        double eps, double* out, int flags) {
     return guard([&] {
+        require_whole(g, "tpa_query_na_batch");
         std::lock_guard<std::mutex> lk(g->mu);
         DeviceGuard dg(g->device);
         // TpaParams::validate (tpa.cpp:8-17)
@@ -1618,3 +1698,5 @@ int tpa_query_na_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, uint32_t
 }
 
 }  // extern "C"
+
+#include "tpa_part.cuh"

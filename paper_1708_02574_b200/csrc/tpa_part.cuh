@@ -1,0 +1,607 @@
+// tpa_part.cuh -- row-partitioned CPI across GPUs (the north star's multi-GPU
+// layout): B = 1 runs (PageRank / preprocess / cpi_run) over a CSR(Ãᵀ) whose
+// rows are split into nnz-balanced ranges, one per GPU, with one exchange per
+// sweep:
+//   * every partition sweeps its own rows with the unchanged K2 kernel
+//     (cpi_spmv2.cuh), reading the full share vector (padded global layout,
+//     PartInfo) and writing its own slice of the next one;
+//   * the residual / dangling totals are exact fixed-point integers, so the
+//     all-reduce of their limbs gives every partition the one-GPU totals bit
+//     for bit, and k_part_finalize advances the same ColState everywhere;
+//   * the share slices are all-gathered in place.
+// Two transports with one driver (run_cpi_part):
+//   * one process per GPU: NCCL (ncclAllReduce of 6 uint64 + in-place
+//     ncclAllGather of the slice) on the partition's stream;
+//   * one process driving all partitions (tpa_group): stream-ordered peer
+//     copies (cudaMemcpyPeerAsync) and a limb-sum kernel, no host sync.
+// Included at the end of tpa_gpu.cu.
+#pragma once
+
+#include <dlfcn.h>
+
+namespace tpa {
+
+// NCCL is resolved at first use, not linked: a process that imports torch
+// after this library must still get torch's own libnccl.so.2 (same soname).
+// An already-loaded libnccl.so.2 (torch's) is reused; else TPA_NCCL_LIB or
+// the system library is opened.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) GetUniqueId;
+    decltype(&ncclCommInitRank) CommInitRank;
+    decltype(&ncclAllReduce) AllReduce;
+    decltype(&ncclAllGather) AllGather;
+    decltype(&ncclCommDestroy) CommDestroy;
+    decltype(&ncclGetErrorString) GetErrorString;
+};
+
+static const NcclApi& nccl() {
+    static std::mutex mu;
+    static NcclApi api{};
+    static bool loaded = false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (loaded) return api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) {
+        const char* e = std::getenv("TPA_NCCL_LIB");
+        h = dlopen(e ? e : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) throw std::runtime_error(std::string("NCCL unavailable: ") + dlerror());
+    auto sym = [&](const char* name) {
+        void* f = dlsym(h, name);
+        if (!f) throw std::runtime_error(std::string("NCCL symbol missing: ") + name);
+        return f;
+    };
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    loaded = true;
+    return api;
+}
+
+#define NCK(x)                                                                                            \
+    do {                                                                                                  \
+        const ncclResult_t r_ = (x);                                                                      \
+        if (r_ != ncclSuccess) throw cuda_error(std::string(#x) + ": " + nccl().GetErrorString(r_));      \
+    } while (0)
+
+static void part_comm_destroy(ncclComm_t c) {
+    if (c) nccl().CommDestroy(c);
+}
+
+__global__ void k_indeg(const uint32_t* __restrict__ tgt, uint64_t m, uint32_t* __restrict__ indeg) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(indeg + tgt[e], 1u);
+}
+
+// Sort keys for partition [lo, hi): local row of in-range edges (others sort
+// last), value = the source's index in the padded share layout.
+__global__ void k_part_keys(const uint32_t* __restrict__ tgt, const uint32_t* __restrict__ src, uint64_t m,
+                            uint32_t lo, uint32_t hi, const uint32_t* __restrict__ bounds, uint32_t G,
+                            uint32_t S, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = tgt[e];
+        if (t >= lo && t < hi) {
+            const uint32_t u = src[e];
+            uint32_t a = 0, b = G;  // largest r with bounds[r] <= u (skips empty partitions)
+            while (b - a > 1) {
+                const uint32_t mid = (a + b) >> 1;
+                if (bounds[mid] <= u) a = mid;
+                else b = mid;
+            }
+            keys[e] = t - lo;
+            vals[e] = a * S + (u - bounds[a]);
+        } else {
+            keys[e] = 0xffffffffu;
+            vals[e] = 0u;
+        }
+    }
+}
+
+struct LimbPtrs {
+    const unsigned long long* p[64];
+};
+
+__global__ void k_sum_limbs(LimbPtrs src, uint32_t G, unsigned long long* __restrict__ total) {
+    const int k = threadIdx.x;
+    if (k >= 6) return;
+    unsigned long long s = 0;
+    for (uint32_t r = 0; r < G; ++r) s += src.p[r][k];
+    total[k] = s;
+}
+
+// Row boundaries balanced by nnz: boundary k is the first row whose in-degree
+// prefix reaches floor(m*k/G) (partition.py restates this for the tests).
+static std::vector<uint32_t> partition_rows(const std::vector<uint64_t>& prefix, uint32_t n, uint32_t G) {
+    const uint64_t m = prefix[n];
+    std::vector<uint32_t> b(G + 1, 0);
+    b[G] = n;
+    for (uint32_t k = 1; k < G; ++k) {
+        const uint64_t target = (uint64_t)((unsigned __int128)m * k / G);
+        const uint32_t v = (uint32_t)(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+        b[k] = std::min(n, std::max(b[k - 1], v));
+    }
+    return b;
+}
+
+// Partition `rank` of `nranks` of the graph given by its out-CSR.
+static void build_part(tpa_graph* g, uint32_t n, uint64_t m, const uint64_t* out_offsets,
+                       const uint32_t* out_targets, uint32_t nranks, uint32_t rank) {
+    cudaStream_t s = g->stream;
+    const int blocks = 8 * g->num_sms;
+    DevBuf d_off, d_tgt, d_src, d_keys, d_vals, d_keys2, d_vals2, d_indeg, d_bounds;
+    d_off.ensure((n + 1ull) * 8, s);
+    d_tgt.ensure(std::max<uint64_t>(m, 1) * 4, s);
+    d_indeg.ensure((size_t)n * 4, s);
+    CK(cudaMemcpyAsync(d_off.p, out_offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
+    if (m) CK(cudaMemcpyAsync(d_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(d_indeg.p, 0, (size_t)n * 4, s));
+    k_indeg<<<blocks, 256, 0, s>>>(d_tgt.as<uint32_t>(), m, d_indeg.as<uint32_t>());
+    CKL("k_indeg");
+    std::vector<uint32_t> indeg(n);
+    CK(cudaMemcpyAsync(indeg.data(), d_indeg.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<uint64_t> prefix(n + 1ull, 0);
+    for (uint32_t v = 0; v < n; ++v) prefix[v + 1] = prefix[v] + indeg[v];
+
+    auto P = std::make_unique<PartInfo>();
+    P->nranks = nranks;
+    P->rank = rank;
+    P->n_global = n;
+    P->m_global = m;
+    P->bounds = partition_rows(prefix, n, nranks);
+    uint32_t S = 1;
+    for (uint32_t r = 0; r < nranks; ++r) S = std::max(S, P->rows(r));
+    P->slice = S;
+    const uint32_t lo = P->bounds[rank], hi = P->bounds[rank + 1], nl = hi - lo;
+    const uint64_t ml = prefix[hi] - prefix[lo];
+
+    d_src.ensure(std::max<uint64_t>(m, 1) * 4, s);
+    d_keys.ensure(std::max<uint64_t>(m, 1) * 4, s);
+    d_vals.ensure(std::max<uint64_t>(m, 1) * 4, s);
+    d_keys2.ensure(std::max<uint64_t>(m, 1) * 4, s);
+    d_vals2.ensure(std::max<uint64_t>(m, 1) * 4, s);
+    d_bounds.ensure((nranks + 1ull) * 4, s);
+    CK(cudaMemcpyAsync(d_bounds.p, P->bounds.data(), (nranks + 1ull) * 4, cudaMemcpyHostToDevice, s));
+    k_expand_src<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>(), n, d_src.as<uint32_t>());
+    CKL("k_expand_src");
+    k_part_keys<<<blocks, 256, 0, s>>>(d_tgt.as<uint32_t>(), d_src.as<uint32_t>(), m, lo, hi,
+                                       d_bounds.as<uint32_t>(), nranks, S, d_keys.as<uint32_t>(),
+                                       d_vals.as<uint32_t>());
+    CKL("k_part_keys");
+    if (m) {
+        // stable: the out-CSR order (ascending source) survives within a row
+        size_t temp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, d_keys.as<uint32_t>(), d_keys2.as<uint32_t>(),
+                                           d_vals.as<uint32_t>(), d_vals2.as<uint32_t>(), (int64_t)m, 0, 32, s));
+        DevBuf d_temp;
+        d_temp.ensure(temp, s);
+        CK(cub::DeviceRadixSort::SortPairs(d_temp.p, temp, d_keys.as<uint32_t>(), d_keys2.as<uint32_t>(),
+                                           d_vals.as<uint32_t>(), d_vals2.as<uint32_t>(), (int64_t)m, 0, 32, s));
+    }
+    g->col.ensure(std::max<uint64_t>(ml, 1) * 4, g->stream);
+    if (ml) CK(cudaMemcpyAsync(g->col.p, d_vals2.p, ml * 4, cudaMemcpyDeviceToDevice, s));
+    g->row_ptr.ensure((nl + 1ull) * 8, g->stream);
+    k_row_ptr<<<blocks, 256, 0, s>>>(d_keys2.as<uint32_t>(), ml, nl, g->row_ptr.as<int64_t>());
+    CKL("k_row_ptr");
+    g->deg.ensure(std::max<size_t>((size_t)nl, 1) * 4, g->stream);
+    if (nl) k_degrees<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>() + lo, nl, g->deg.as<uint32_t>());
+    CKL("k_degrees");
+    std::vector<int64_t> rp(nl + 1ull);
+    CK(cudaMemcpyAsync(rp.data(), g->row_ptr.p, (nl + 1ull) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    g->launches += 6;
+    g->n = nl;
+    g->m = ml;
+    g->part = std::move(P);
+    build_schedules(g, rp, nl);
+}
+
+struct PartRun {
+    double c = 0.15, eps = 1e-9;
+    uint32_t start = 0;
+    int64_t terminal = -1;
+    const std::vector<uint32_t>* seeds = nullptr;  // sorted, unique; null: all nodes (PageRank)
+    double* out = nullptr;                         // n_global scores (host, or device via UVA)
+    ColState state{};
+};
+
+static unsigned long long* limbs_slot(Workspace& w, int slot) { return w.limbs.as<unsigned long long>() + slot * 6; }
+static unsigned long long* limbs_total(Workspace& w) { return w.limbs.as<unsigned long long>() + 18; }
+
+// All-reduce the limbs of `slot` into every partition's totals, then (share
+// >= 0) all-gather share buffer `share`.  Stream-ordered, no host sync.
+static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share) {
+    const uint32_t G = Pg[0]->part->nranks;
+    if (Pg.size() == 1) {
+        tpa_graph* g = Pg[0];
+        Workspace& w = g->workspace(1);
+        PartInfo& P = *g->part;
+        if (P.comm) {
+            NCK(nccl().AllReduce(limbs_slot(w, slot), limbs_total(w), 6, ncclUint64, ncclSum, P.comm, g->stream));
+            if (share >= 0) {
+                double* buf = w.share[share].as<double>();
+                NCK(nccl().AllGather(buf + (size_t)P.rank * P.slice, buf, P.slice, ncclDouble, P.comm, g->stream));
+            }
+        } else {
+            CK(cudaMemcpyAsync(limbs_total(w), limbs_slot(w, slot), 48, cudaMemcpyDeviceToDevice, g->stream));
+        }
+        return;
+    }
+    // in-process group: every partition waits for every partition's sweep
+    std::vector<cudaEvent_t> ev(G);
+    for (uint32_t r = 0; r < G; ++r) {
+        DeviceGuard dg(Pg[r]->device);
+        ev[r] = Pg[r]->take_event();
+        CK(cudaEventRecord(ev[r], Pg[r]->stream));
+    }
+    LimbPtrs lp{};
+    for (uint32_t r = 0; r < G; ++r) lp.p[r] = limbs_slot(Pg[r]->workspace(1), slot);
+    for (uint32_t q = 0; q < G; ++q) {
+        tpa_graph* g = Pg[q];
+        DeviceGuard dg(g->device);
+        for (uint32_t r = 0; r < G; ++r) CK(cudaStreamWaitEvent(g->stream, ev[r], 0));
+        Workspace& w = g->workspace(1);
+        k_sum_limbs<<<1, 32, 0, g->stream>>>(lp, G, limbs_total(w));
+        CKL("k_sum_limbs");
+        ++g->launches;
+        if (share >= 0) {
+            const PartInfo& P = *g->part;
+            for (uint32_t r = 0; r < G; ++r) {
+                if (r == q || P.rows(r) == 0) continue;
+                double* dst = w.share[share].as<double>() + (size_t)r * P.slice;
+                const double* src = Pg[r]->workspace(1).share[share].as<double>() + (size_t)r * P.slice;
+                CK(cudaMemcpyPeerAsync(dst, g->device, src, Pg[r]->device, (size_t)P.rows(r) * 8, g->stream));
+            }
+        }
+    }
+    // the events are reusable once the waits are enqueued
+    for (uint32_t r = 0; r < G; ++r) Pg[r]->event_pool.push_back(ev[r]);
+}
+
+// cpi_run / pagerank / preprocess over a row partition (B = 1).  All
+// partitions run the same sweep sequence: the state they read back is the
+// same (exact all-reduced totals).
+static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
+    const uint32_t G = Pg[0]->part->nranks;
+    const uint32_t n = Pg[0]->part->n_global;
+    const double keep = 1.0 - cfg.c;
+    const int active0 = cfg.terminal != 0;
+    std::vector<DevBuf> dx(Pg.size());
+    std::vector<StepArgs> A(Pg.size());
+    // x⁰ (cpi.cpp:59-63), accumulated iff the window starts at 0
+    for (size_t k = 0; k < Pg.size(); ++k) {
+        tpa_graph* g = Pg[k];
+        DeviceGuard dg(g->device);
+        Workspace& w = g->workspace(1);
+        w.limbs.ensure(24 * 8, g->stream);
+        const PartInfo& P = *g->part;
+        const uint32_t nl = g->n, lo = P.row_begin();
+        double* acc0 = cfg.start == 0 ? w.acc.as<double>() : nullptr;
+        if (!acc0 && nl) CK(cudaMemsetAsync(w.acc.p, 0, (size_t)nl * 8, g->stream));
+        double weight = cfg.c / (double)n;
+        if (cfg.seeds) {
+            std::vector<double> x0(std::max<uint32_t>(nl, 1), 0.0);
+            const double wgt = cfg.c / (double)cfg.seeds->size();
+            for (uint32_t sd : *cfg.seeds)
+                if (sd >= lo && sd < lo + nl) x0[sd - lo] = wgt;
+            dx[k].ensure(x0.size() * 8, g->stream);
+            CK(cudaMemcpyAsync(dx[k].p, x0.data(), x0.size() * 8, cudaMemcpyHostToDevice, g->stream));
+            CK(cudaStreamSynchronize(g->stream));  // x0 is a local
+        }
+        if (nl) {
+            const int nblk = grid_for(nl, 4 * kThreads, 4 * g->num_sms);
+            k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.seeds ? dx[k].as<double>() : nullptr, weight, nl,
+                                                           g->deg.as<uint32_t>(), keep,
+                                                           w.share[0].as<double>() + (size_t)P.rank * P.slice,
+                                                           acc0, w.fx.as<unsigned long long>());
+            CKL("k_init_dense");
+        }
+        k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), limbs_slot(w, 2), g->policy, keep, n,
+                                              active0, w.state.as<ColState>());
+        CKL("k_init_finish");
+        g->launches += 2;
+        StepArgs& a = A[k];
+        a = StepArgs{};
+        a.row_ptr = g->row_ptr.as<int64_t>();
+        a.col = g->col.as<uint32_t>();
+        a.deg = g->deg.as<uint32_t>();
+        a.items = g->mv.items.as<uint2>();
+        a.n_items = g->mv.n_items;
+        a.n = n;  // the graph's n: Uniform spread (graph.cpp:265-268)
+        a.policy = g->policy;
+        a.keep = keep;
+        a.eps = cfg.eps;
+        a.terminal = cfg.terminal;
+        a.scale = 1.0;
+        a.b_valid = 1;
+        a.part = w.part.as<double>();
+        a.gpart = w.gpart.as<double>();
+        a.group_cnt = w.group_cnt.as<uint32_t>();
+        a.done_cnt = w.done_cnt.as<uint32_t>();
+    }
+    part_exchange(Pg, 2, 0);
+    for (size_t k = 0; k < Pg.size(); ++k) {
+        tpa_graph* g = Pg[k];
+        DeviceGuard dg(g->device);
+        Workspace& w = g->workspace(1);
+        StepArgs a = A[k];
+        a.state_out = w.state.as<ColState>();
+        k_part_finalize<<<1, 1, 0, g->stream>>>(limbs_total(w), a, 1, active0);
+        CKL("k_part_finalize");
+        ++g->launches;
+    }
+
+    const int64_t target = cfg.terminal >= 0 ? cfg.terminal : std::numeric_limits<int64_t>::max();
+    const uint32_t est = sweeps_estimate(cfg.c, cfg.eps);
+    uint64_t done = 0;
+    int64_t chunk = std::min<int64_t>(target, (int64_t)est + 1);
+    ColState hst{};
+    while (chunk > 0) {
+        for (int64_t j = 0; j < chunk; ++j) {
+            const uint32_t i = (uint32_t)(done + 1 + j);
+            const bool last = (int64_t)i == target;
+            const bool inw = i >= cfg.start && (cfg.terminal < 0 || (int64_t)i <= cfg.terminal);
+            for (size_t k = 0; k < Pg.size(); ++k) {
+                tpa_graph* g = Pg[k];
+                DeviceGuard dg(g->device);
+                Workspace& w = g->workspace(1);
+                const PartInfo& P = *g->part;
+                StepArgs& a = A[k];
+                ColState* st = w.state.as<ColState>();
+                a.step = i;
+                a.share_in = w.share[(i - 1) & 1].as<double>();
+                a.share_out = last ? nullptr : w.share[i & 1].as<double>() + (size_t)P.rank * P.slice;
+                a.acc = inw ? w.acc.as<double>() : nullptr;
+                a.state_in = st + ((i - 1) & 1);
+                a.state_out = st + (i & 1);
+                if (g->n) launch_step(g, w, a, nullptr, 1);
+                else CK(cudaMemsetAsync(limbs_slot(w, i & 1), 0, 48, g->stream));  // empty partition
+            }
+            part_exchange(Pg, (int)(i & 1), last ? -1 : (int)(i & 1));
+            for (size_t k = 0; k < Pg.size(); ++k) {
+                tpa_graph* g = Pg[k];
+                DeviceGuard dg(g->device);
+                Workspace& w = g->workspace(1);
+                k_part_finalize<<<1, 1, 0, g->stream>>>(limbs_total(w), A[k], 0, 0);
+                CKL("k_part_finalize");
+                ++g->launches;
+            }
+        }
+        done += chunk;
+        if ((int64_t)done >= target) break;
+        tpa_graph* g0 = Pg[0];
+        {
+            DeviceGuard dg(g0->device);
+            CK(cudaMemcpyAsync(&hst, g0->workspace(1).state.as<ColState>() + (done & 1), sizeof(ColState),
+                               cudaMemcpyDeviceToHost, g0->stream));
+            CK(cudaStreamSynchronize(g0->stream));
+        }
+        if (!hst.active) break;
+        chunk = std::min<int64_t>(target - (int64_t)done, 16);
+    }
+    // the accumulators, assembled into the caller's n-vector
+    for (size_t k = 0; k < Pg.size(); ++k) {
+        tpa_graph* g = Pg[k];
+        DeviceGuard dg(g->device);
+        Workspace& w = g->workspace(1);
+        const PartInfo& P = *g->part;
+        if (Pg.size() == 1 && P.comm) {
+            DevBuf pad;
+            pad.ensure((size_t)G * P.slice * 8, g->stream);
+            if (g->n)
+                CK(cudaMemcpyAsync(pad.as<double>() + (size_t)P.rank * P.slice, w.acc.p, (size_t)g->n * 8,
+                                   cudaMemcpyDeviceToDevice, g->stream));
+            NCK(nccl().AllGather(pad.as<double>() + (size_t)P.rank * P.slice, pad.as<double>(), P.slice, ncclDouble,
+                              P.comm, g->stream));
+            for (uint32_t r = 0; r < G; ++r)
+                if (P.rows(r))
+                    CK(cudaMemcpyAsync(cfg.out + P.bounds[r], pad.as<double>() + (size_t)r * P.slice,
+                                       (size_t)P.rows(r) * 8, cudaMemcpyDefault, g->stream));
+        } else if (g->n) {
+            CK(cudaMemcpyAsync(cfg.out + P.row_begin(), w.acc.p, (size_t)g->n * 8, cudaMemcpyDefault, g->stream));
+        }
+        CK(cudaMemcpyAsync(&cfg.state, w.state.as<ColState>() + (done & 1), sizeof(ColState),
+                           cudaMemcpyDeviceToHost, g->stream));
+    }
+    for (tpa_graph* g : Pg) {
+        DeviceGuard dg(g->device);
+        CK(cudaStreamSynchronize(g->stream));
+    }
+}
+
+}  // namespace tpa
+
+struct tpa_group {
+    std::vector<tpa_graph*> parts;
+    std::mutex mu;
+};
+
+namespace tpa {
+
+static void require_whole(const tpa_graph* g, const char* what) {
+    if (g->part)
+        throw std::invalid_argument(std::string(what) +
+                                    " is not available on a row-partitioned graph (use a whole-graph replica)");
+}
+
+static void part_cpi_run(std::vector<tpa_graph*>& Pg, const uint32_t* seeds, uint64_t n_seeds, double c,
+                         double eps, uint32_t start_iter, int64_t terminal_iter, double* out_scores,
+                         uint32_t* iterations_run, int* converged, double* residual_l1) {
+    const uint32_t n = Pg[0]->part->n_global;
+    std::vector<uint32_t> hs;
+    if (seeds) {
+        if (n_seeds == 0) throw std::invalid_argument("seed set must not be empty");
+        hs.assign(seeds, seeds + n_seeds);
+        std::sort(hs.begin(), hs.end());
+        if (std::adjacent_find(hs.begin(), hs.end()) != hs.end())
+            throw std::invalid_argument("seed set contains duplicate ids");
+    }
+    validate_cpi(c, eps, start_iter, terminal_iter);
+    if (seeds) validate_seed(hs.back(), n);
+    if (!out_scores) throw std::invalid_argument("null output");
+    PartRun cfg;
+    cfg.c = c;
+    cfg.eps = eps;
+    cfg.start = start_iter;
+    cfg.terminal = terminal_iter;
+    cfg.seeds = seeds ? &hs : nullptr;
+    cfg.out = out_scores;
+    run_cpi_part(Pg, cfg);
+    if (iterations_run) *iterations_run = cfg.state.iters;
+    if (converged) *converged = cfg.state.converged;
+    if (residual_l1) *residual_l1 = cfg.state.residual;
+}
+
+static void part_preprocess(std::vector<tpa_graph*>& Pg, double c, double eps, uint32_t T, double* out) {
+    if (T < 1) throw std::invalid_argument("stranger_start (T) must be at least 1");  // tpa.cpp:21-22
+    validate_cpi(c, eps, T, -1);
+    if (!out) throw std::invalid_argument("null output");
+    PartRun cfg;
+    cfg.c = c;
+    cfg.eps = eps;
+    cfg.start = T;
+    cfg.terminal = -1;
+    cfg.out = out;
+    run_cpi_part(Pg, cfg);
+}
+
+}  // namespace tpa
+
+namespace tpa {
+
+static tpa_graph* make_part_graph(uint32_t n, uint64_t m, const uint64_t* out_offsets, const uint32_t* out_targets,
+                                  int policy, uint64_t fingerprint, int device, uint32_t nranks, uint32_t rank) {
+    if (n == 0) throw std::invalid_argument("graph must have at least one node");
+    if (policy < 0 || policy > 2) throw std::invalid_argument("unknown dangling policy");
+    if (!out_offsets || (m && !out_targets)) throw std::invalid_argument("null graph arrays");
+    if (out_offsets[n] != m) throw std::invalid_argument("out_offsets[n] != m");
+    if (nranks == 0 || rank >= nranks) throw std::invalid_argument("rank must be in [0, nranks)");
+    DeviceGuard dg(device);
+    auto g = std::make_unique<tpa_graph>();
+    g->device = device;
+    g->policy = policy;
+    g->fingerprint = fingerprint;
+    CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->own_stream = true;
+    build_part(g.get(), n, m, out_offsets, out_targets, nranks, rank);
+    return g.release();
+}
+
+}  // namespace tpa
+
+extern "C" {
+
+int tpa_comm_unique_id(void* id_out) {
+    return guard([&] {
+        if (!id_out) throw std::invalid_argument("null output");
+        ncclUniqueId id;
+        NCK(nccl().GetUniqueId(&id));
+        static_assert(sizeof(ncclUniqueId) == TPA_COMM_ID_BYTES, "NCCL unique id size");
+        std::memcpy(id_out, &id, sizeof(id));
+    });
+}
+
+int tpa_graph_create_part(uint32_t n, uint64_t m, const uint64_t* out_offsets, const uint32_t* out_targets,
+                          int policy, uint64_t fingerprint, int device, uint32_t nranks, uint32_t rank,
+                          const void* comm_id, tpa_graph** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output handle");
+        if (nranks > 1 && !comm_id)
+            throw std::invalid_argument("nranks > 1 needs a communicator id (tpa_comm_unique_id) or tpa_group_create");
+        std::unique_ptr<tpa_graph, int (*)(tpa_graph*)> g(
+            make_part_graph(n, m, out_offsets, out_targets, policy, fingerprint, device, nranks, rank),
+            tpa_graph_destroy);
+        if (comm_id) {
+            DeviceGuard dg(device);
+            ncclUniqueId id;
+            std::memcpy(&id, comm_id, sizeof(id));
+            NCK(nccl().CommInitRank(&g->part->comm, (int)nranks, id, (int)rank));
+        }
+        *out = g.release();
+    });
+}
+
+int tpa_graph_part_info(const tpa_graph* g, uint32_t* nranks, uint32_t* rank, uint32_t* row_begin,
+                        uint32_t* row_end, uint32_t* slice) {
+    return guard([&] {
+        if (!g) throw std::invalid_argument("null graph");
+        const PartInfo* P = g->part.get();
+        if (nranks) *nranks = P ? P->nranks : 1;
+        if (rank) *rank = P ? P->rank : 0;
+        if (row_begin) *row_begin = P ? P->row_begin() : 0;
+        if (row_end) *row_end = P ? P->bounds[P->rank + 1] : g->n;
+        if (slice) *slice = P ? P->slice : g->n;
+    });
+}
+
+int tpa_group_create(uint32_t n, uint64_t m, const uint64_t* out_offsets, const uint32_t* out_targets, int policy,
+                     uint64_t fingerprint, const int* devices, uint32_t nparts, tpa_group** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null output handle");
+        if (nparts == 0 || nparts > 64) throw std::invalid_argument("a group has 1..64 partitions");
+        if (!devices) throw std::invalid_argument("null device list");
+        auto grp = std::make_unique<tpa_group>();
+        try {
+            for (uint32_t r = 0; r < nparts; ++r)
+                grp->parts.push_back(
+                    make_part_graph(n, m, out_offsets, out_targets, policy, fingerprint, devices[r], nparts, r));
+            // peer access between distinct devices (copies and the limb sum read peers)
+            for (uint32_t a = 0; a < nparts; ++a)
+                for (uint32_t b = 0; b < nparts; ++b) {
+                    if (devices[a] == devices[b]) continue;
+                    DeviceGuard dg(devices[a]);
+                    int ok = 0;
+                    CK(cudaDeviceCanAccessPeer(&ok, devices[a], devices[b]));
+                    if (!ok) throw std::invalid_argument("group devices lack peer access");
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                    cudaGetLastError();
+                }
+        } catch (...) {
+            for (tpa_graph* g : grp->parts) tpa_graph_destroy(g);
+            throw;
+        }
+        *out = grp.release();
+    });
+}
+
+int tpa_group_destroy(tpa_group* grp) {
+    return guard([&] {
+        if (!grp) return;
+        for (tpa_graph* g : grp->parts) tpa_graph_destroy(g);
+        delete grp;
+    });
+}
+
+int tpa_group_part(tpa_group* grp, uint32_t r, tpa_graph** out) {
+    return guard([&] {
+        if (!grp || !out) throw std::invalid_argument("null handle");
+        if (r >= grp->parts.size()) throw std::out_of_range("partition index out of range");
+        *out = grp->parts[r];
+    });
+}
+
+int tpa_group_cpi_run(tpa_group* grp, const uint32_t* seeds, uint64_t n_seeds, double c, double eps,
+                      uint32_t start_iter, int64_t terminal_iter, double* out_scores, uint32_t* iterations_run,
+                      int* converged, double* residual_l1) {
+    return guard([&] {
+        if (!grp) throw std::invalid_argument("null group");
+        std::lock_guard<std::mutex> lk(grp->mu);
+        part_cpi_run(grp->parts, seeds, n_seeds, c, eps, start_iter, terminal_iter, out_scores, iterations_run,
+                     converged, residual_l1);
+    });
+}
+
+int tpa_group_preprocess(tpa_group* grp, double c, double eps, uint32_t T, double* out_stranger) {
+    return guard([&] {
+        if (!grp) throw std::invalid_argument("null group");
+        std::lock_guard<std::mutex> lk(grp->mu);
+        part_preprocess(grp->parts, c, eps, T, out_stranger);
+    });
+}
+
+}  // extern "C"

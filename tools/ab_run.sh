@@ -1,5 +1,2 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python tools/ab_time.py c2 32 2>&1 | grep -E "sweep |ms/batch"
-TPA_SPARSE_DIV=8 python tools/ab_time.py c2 32 2>&1 | grep -E "sweep |ms/batch"
-python tools/ab_time.py c3 64 2>&1 | grep -E "sweep |ms/batch"
-ncu --metrics gpu__time_duration.sum --clock-control none -s 150 -c 60 --csv --log-file gpurun_out/ll_def.csv python tools/profile_step.py --batches 3 > /dev/null 2>&1
+for v in "" "TPA_MV_CARVEOUT=25" "TPA_MV_CARVEOUT=40" "TPA_MV_CARVEOUT=50" "TPA_MV_CARVEOUT=60" "TPA_MV_CARVEOUT=100"; do
+echo "== $v"; env $v python tools/ab_time.py c2 32 2>&1 | grep -E "spmv"; done

@@ -11,7 +11,7 @@ import build as B  # noqa: E402
 name, extra = sys.argv[1], sys.argv[2:]
 os.makedirs(os.path.join(ROOT, "tools", "bin"), exist_ok=True)
 out = os.path.join(ROOT, "tools", "bin", f"libtpa_{name}.so")
-cmd = ["nvcc", *B.NVCC_FLAGS, *extra, "-shared", "-I", B.INCLUDE, "-I", B.CSRC, "-o", out, *B.sources()]
+cmd = ["nvcc", *B.NVCC_FLAGS, *extra, "-shared", "-I", B.INCLUDE, "-I", B.CSRC, "-o", out, *B.sources(), *B.LIBS]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
     sys.exit(r.stderr)
