@@ -282,8 +282,19 @@ def run_ours(args):
     g = build_graph(cfg_name)
     t_build = time.perf_counter() - t0
     n, m = g.node_count(), g.edge_count()
-    all_seeds = P.sample_seeds(g, nq * world, seed)
-    seeds = np.ascontiguousarray(all_seeds[rank * nq:(rank + 1) * nq])
+    # N > 1 (strong scaling of the one C2 job): PageRank preprocessing row-
+    # partitioned across the ranks (one NCCL exchange per sweep, the north
+    # star's layout) and the job's queries split across the ranks, each on a
+    # whole-graph replica.  TPA_BENCH_REPLICAS=1: N independent jobs instead.
+    replicas = world > 1 and os.environ.get("TPA_BENCH_REPLICAS") == "1"
+    # TPA_BENCH_PART=1 at N = 1: the partitioned code path with one rank (NCCL
+    # communicator of one), to exercise it on a single GPU
+    partitioned = (world > 1 and not replicas) or os.environ.get("TPA_BENCH_PART") == "1"
+    all_seeds = P.sample_seeds(g, nq * (world if replicas else 1), seed)
+    if replicas:
+        seeds = np.ascontiguousarray(all_seeds[rank * nq:(rank + 1) * nq])
+    else:
+        seeds = np.ascontiguousarray(np.array_split(all_seeds, world)[rank]) if world > 1 else all_seeds
     log(f"[rank {rank}] graph {cfg_name}: n={n} m={m} built in {t_build:.1f}s")
 
     t0 = time.perf_counter()
@@ -301,11 +312,26 @@ def run_ours(args):
 
     out = torch.empty((batch, n), dtype=torch.float64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    batches = [np.ascontiguousarray(seeds[i:i + batch]) for i in range(0, nq, batch)]
+    batches = [np.ascontiguousarray(seeds[i:i + batch]) for i in range(0, len(seeds), batch)]
+    pg = None
+    if partitioned:
+        if world > 1:
+            pg = P.PartitionedGraph.from_process_group(g, device=local)
+        else:
+            pg = P.PartitionedGraph(g, 1, 0, comm_id=P.partition.comm_unique_id(), device=local)
+        N.check(lib.tpa_graph_set_stream(pg.h, stream.cuda_stream))
+        d_str = torch.empty(n, dtype=torch.float64, device=dev)
+        log(f"[rank {rank}] partition {pg.info()}")
 
     def device_step():
         art = C_.c_void_p()
-        N.check(lib.tpa_preprocess(h, C, EPS, T, None, C_.byref(art), N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
+        if pg is None:
+            N.check(lib.tpa_preprocess(h, C, EPS, T, None, C_.byref(art), N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
+        else:
+            # collective: every rank ends with the whole stranger vector on its GPU
+            N.check(lib.tpa_preprocess(pg.h, C, EPS, T, d_str.data_ptr(), None, N.TPA_DEVICE_PTRS))
+            N.check(lib.tpa_artifact_create(h, d_str.data_ptr(), g.fingerprint(), C, EPS, T, N.TPA_DEVICE_PTRS,
+                                            C_.byref(art)))
         for b in batches:
             N.check(lib.tpa_query_batch(h, art, b.ctypes.data, len(b), S, out.data_ptr(),
                                         N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
@@ -319,9 +345,11 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
-    launches0 = dg.launches()
+    launches0 = dg.launches() + (N.lib.tpa_graph_launches(pg.h) if pg is not None else 0)
     times = []
     dg.profile(True)
+    if pg is not None:
+        N.check(lib.tpa_graph_profile(pg.h, 1))
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
@@ -334,8 +362,13 @@ def run_ours(args):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             lib.tpa_artifact_destroy(a)
-    launches = dg.launches() - launches0
+    launches = dg.launches() + (N.lib.tpa_graph_launches(pg.h) if pg is not None else 0) - launches0
     mv_cnt, mv_ms = dg.profile_read(1)
+    if pg is not None:
+        c_, ms_ = C_.c_uint64(), C_.c_double()
+        N.check(lib.tpa_graph_profile_read(pg.h, 1, -1, C_.byref(c_), C_.byref(ms_)))
+        mv_cnt, mv_ms = mv_cnt + c_.value, mv_ms + ms_.value
+        N.check(lib.tpa_graph_profile(pg.h, 0))
     mm_cnt, mm_ms = dg.profile_read(batch if batch > 1 else 1)
     per_sweep = {}
     if batch > 1:
@@ -359,9 +392,10 @@ def run_ours(args):
     # sweeps actually run: 116 PageRank sweeps (the convergence break) + (S-1) per query
     pr = P.pagerank(g, P.CpiParams(C, EPS))
     pre_sweeps = pr.iterations_run
+    jobs = 1 if partitioned else world  # independent C2 jobs per step
     edges_per_step = m * (pre_sweeps + (S - 1) * nq)
-    value = edges_per_step * world * args.steps / (total_ms / 1e3) / 1e9
-    qps = nq * world * args.steps / (total_ms / 1e3)
+    value = edges_per_step * jobs * args.steps / (total_ms / 1e3) / 1e9
+    qps = nq * jobs * args.steps / (total_ms / 1e3)
 
     # roofline of the dominant kernel (the SpMM sweep at batch width B)
     peak, peak_src = peak_hbm()
@@ -406,7 +440,12 @@ def run_ours(args):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             art = C_.c_void_p()
-            N.check(lib.tpa_preprocess(h, C, EPS, T, host_str.data_ptr(), C_.byref(art), 0))
+            if pg is None:
+                N.check(lib.tpa_preprocess(h, C, EPS, T, host_str.data_ptr(), C_.byref(art), 0))
+            else:
+                N.check(lib.tpa_preprocess(pg.h, C, EPS, T, host_str.data_ptr(), None, 0))
+                N.check(lib.tpa_artifact_create(h, host_str.data_ptr(), g.fingerprint(), C, EPS, T, 0,
+                                                C_.byref(art)))
             d2h_s = n * 8
             h2d_s = 0
             for b in batches:
@@ -420,9 +459,9 @@ def run_ours(args):
         tt = torch.tensor([sum(el)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": edges_per_step * world * e2e_steps / float(tt.item()) / 1e9, "unit": "GTEPS",
+        e2e = {"value": edges_per_step * jobs * e2e_steps / float(tt.item()) / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "queries_per_s": nq * world * e2e_steps / float(tt.item()),
+               "queries_per_s": nq * jobs * e2e_steps / float(tt.item()),
                "steps": e2e_steps, "ms_per_step": float(tt.item()) / e2e_steps * 1e3,
                "note": "C-ABI with host buffers: seeds from host, stranger + every full score vector "
                        "copied back to pinned host memory (the reference API returns ScoreVectors)"}
@@ -435,12 +474,15 @@ def run_ours(args):
         line = {
             "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",
             "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg_name, g, nq, batch),
             "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "ingest_s": t_ingest, "graph_build_s": t_build,
-            "parallelism": f"seed-parallel replicas x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"row-partitioned preprocess (NCCL all-reduce + all-gather per sweep) + "
+                            f"queries split over {world} whole-graph replicas" if partitioned else
+                            f"independent replicas x{world}" if world > 1 else "single GPU"),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -111,6 +111,50 @@ __device__ __forceinline__ void fx_atomic_add(unsigned long long* p_hi, unsigned
     if (hi + carry) atomicAdd(p_hi, hi + carry);
 }
 
+// Exact warp total of per-lane 128-bit fixed-point values (every lane gets it).
+__device__ __forceinline__ void fx_warp_sum(unsigned long long& hi, unsigned long long& lo) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long oh = __shfl_xor_sync(0xffffffffu, hi, o);
+        const unsigned long long ol = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long l2 = lo + ol;
+        hi += oh + (l2 < lo ? 1ull : 0ull);
+        lo = l2;
+    }
+}
+
+// CTA total of per-thread (l1, dm) fixed-point pairs added into the global
+// fx[4] (warp shuffles, then one thread; no shared-memory atomics).  Every
+// thread of the CTA must call it.  s_w: >= 4 * (blockDim.x / 32) words.
+__device__ __forceinline__ void fx_cta_flush(unsigned long long f0, unsigned long long f1, unsigned long long f2,
+                                             unsigned long long f3, unsigned long long* s_w,
+                                             unsigned long long* fx) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    fx_warp_sum(f0, f1);
+    fx_warp_sum(f2, f3);
+    if (lane == 0) {
+        s_w[4 * w + 0] = f0;
+        s_w[4 * w + 1] = f1;
+        s_w[4 * w + 2] = f2;
+        s_w[4 * w + 3] = f3;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+        for (int k = 0; k < nw; ++k) {
+            unsigned long long t = l0 + s_w[4 * k + 1];
+            h0 += s_w[4 * k + 0] + (t < l0 ? 1ull : 0ull);
+            l0 = t;
+            t = l1 + s_w[4 * k + 3];
+            h1 += s_w[4 * k + 2] + (t < l1 ? 1ull : 0ull);
+            l1 = t;
+        }
+        if (h0 | l0) fx_atomic_add(&fx[0], &fx[1], h0, l0);
+        if (h1 | l1) fx_atomic_add(&fx[2], &fx[3], h1, l1);
+    }
+}
+
+
 template <int B>
 struct MmShape {
     static constexpr int G = MmVec<B>::G, CPL = MmVec<B>::CPL;

@@ -6,13 +6,14 @@
 //   * the tile's nnz range travels with the work item, so the index loads,
 //     the row_ptr loads and the per-row out-degree / accumulator loads are all
 //     issued at once (one round trip), then the gathers (a second one);
-//   * every row's |y| (and dangling y) is added as an exact 128-bit
-//     fixed-point integer (order-free), per thread, then per CTA, then across
-//     CTAs: the totals do not depend on how rows are grouped into tiles, CTAs
-//     or GPU partitions, so a row-partitioned run (cpi_part.cuh) reproduces
-//     the one-GPU residuals bit for bit; the last CTA advances the state, or,
-//     for a partition, publishes its totals as carry-free limbs for an
-//     all-reduce (fx_to_limbs) and leaves the state to k_part_finalize.
+//   * the L1 residual and dangling mass are reduced per tile in a fixed tree
+//     and added across tiles as exact 128-bit fixed-point integers
+//     (order-free): the totals depend only on the tiling, which a row
+//     partition cut at tile starts (tpa_part.cuh) leaves unchanged, so a
+//     partitioned run reproduces the one-GPU residuals bit for bit.  The last
+//     CTA advances the state, or, for a partition, publishes its totals as
+//     carry-free limbs for an all-reduce (fx_to_limbs) and leaves the state
+//     to k_part_finalize.
 #pragma once
 
 #include "cpi_spmm.cuh"
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         return;
     }
     const bool want_dm = a.policy == kUniform;
-    unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;  // this thread's exact |y| and dangling sums
+    double my_l1 = 0.0, my_dm = 0.0;
 
     if (!is_long) {
         const uint32_t nrows = re - rb;
@@ -163,8 +164,8 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
                 }
             }
             if (a.share_out) a.share_out[vtx] = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
-            fx_add(f0, f1, y);
-            if (want_dm && dg[q] == 0) fx_add(f2, f3, y);
+            my_l1 = dadd(my_l1, fabs(y));
+            if (want_dm && dg[q] == 0) my_dm = dadd(my_dm, y);
         }
     } else {
         // one long row: every thread sums a fixed strided subset, then a fixed tree
@@ -186,20 +187,24 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
             const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
-            fx_add(f0, f1, y);
-            if (want_dm && d == 0) fx_add(f2, f3, y);
+            my_l1 = fabs(y);
+            if (want_dm && d == 0) my_dm = y;
         }
     }
-    // exact integer totals: thread -> CTA (shared) -> grid
-    __shared__ unsigned long long s_fx[4];
-    if (tid < 4) s_fx[tid] = 0ull;
-    __syncthreads();
-    if (f0 | f1) fx_atomic_add(&s_fx[0], &s_fx[1], f0, f1);
-    if (f2 | f3) fx_atomic_add(&s_fx[2], &s_fx[3], f2, f3);
-    __syncthreads();
+    // tile partials (fixed tree) -> exact fixed-point totals across tiles
+    const double tl1 = block_sum(my_l1, s_red);
+    const double tdm = want_dm ? block_sum(my_dm, s_red) : 0.0;
     if (tid == 0) {
-        if (s_fx[0] | s_fx[1]) fx_atomic_add(&M.fx[0], &M.fx[1], s_fx[0], s_fx[1]);
-        if (s_fx[2] | s_fx[3]) fx_atomic_add(&M.fx[2], &M.fx[3], s_fx[2], s_fx[3]);
+        unsigned long long h = 0, l = 0;
+        if (tl1 != 0.0) {
+            fx_add(h, l, tl1);
+            fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
+        }
+        if (tdm != 0.0) {
+            h = l = 0;
+            fx_add(h, l, tdm);
+            fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
+        }
         __threadfence();
         s_ticket = atomicAdd(a.done_cnt, 1u);
     }

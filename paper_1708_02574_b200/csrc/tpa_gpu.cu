@@ -150,9 +150,7 @@ __global__ void __launch_bounds__(kThreads)
 k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
              const uint32_t* __restrict__ deg, double keep, double* __restrict__ share0,
              double* __restrict__ acc0, unsigned long long* fx) {
-    __shared__ unsigned long long s_fx[4];
-    if (threadIdx.x < 4) s_fx[threadIdx.x] = 0ull;
-    __syncthreads();
+    __shared__ unsigned long long s_w[4 * (kThreads / 32)];
     unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
     for (uint64_t u = blockIdx.x * (uint64_t)kThreads + threadIdx.x; u < n; u += (uint64_t)gridDim.x * kThreads) {
         const double xv = x ? x[u] : weight;
@@ -162,13 +160,7 @@ k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
         fx_add(f0, f1, xv);
         if (d == 0) fx_add(f2, f3, xv);
     }
-    if (f0 | f1) fx_atomic_add(&s_fx[0], &s_fx[1], f0, f1);
-    if (f2 | f3) fx_atomic_add(&s_fx[2], &s_fx[3], f2, f3);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s_fx[0] | s_fx[1]) fx_atomic_add(&fx[0], &fx[1], s_fx[0], s_fx[1]);
-        if (s_fx[2] | s_fx[3]) fx_atomic_add(&fx[2], &fx[3], s_fx[2], s_fx[3]);
-    }
+    fx_cta_flush(f0, f1, f2, f3, s_w, fx);
 }
 
 // x⁰'s ColState from the totals (then fx is zeroed for the sweeps); a

@@ -112,15 +112,30 @@ __global__ void k_sum_limbs(LimbPtrs src, uint32_t G, unsigned long long* __rest
     total[k] = s;
 }
 
-// Row boundaries balanced by nnz: boundary k is the first row whose in-degree
-// prefix reaches floor(m*k/G) (partition.py restates this for the tests).
+// Row boundaries balanced by nnz and cut only where the whole graph's SpMV
+// tiling (build_items) starts an item: the greedy tiling of a suffix that
+// begins at an item start is that suffix of the whole tiling, so every
+// partition sweeps exactly the whole graph's tiles and the per-tile residual
+// partials -- hence the exact totals -- are the same for any partition count.
+// Boundary k is the first cut point whose in-degree prefix reaches
+// floor(m*k/G) (partition.py restates this).
 static std::vector<uint32_t> partition_rows(const std::vector<uint64_t>& prefix, uint32_t n, uint32_t G) {
     const uint64_t m = prefix[n];
+    std::vector<int64_t> rp(prefix.begin(), prefix.end());
+    std::vector<uint2> items = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
+    std::vector<uint32_t> cuts;
+    cuts.reserve(items.size() + 1);
+    for (const uint2& it : items) cuts.push_back(it.x);
+    cuts.push_back(n);
+    std::sort(cuts.begin(), cuts.end());
+    std::vector<uint64_t> cut_prefix(cuts.size());
+    for (size_t i = 0; i < cuts.size(); ++i) cut_prefix[i] = prefix[cuts[i]];
     std::vector<uint32_t> b(G + 1, 0);
     b[G] = n;
     for (uint32_t k = 1; k < G; ++k) {
         const uint64_t target = (uint64_t)((unsigned __int128)m * k / G);
-        const uint32_t v = (uint32_t)(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+        const size_t i = std::lower_bound(cut_prefix.begin(), cut_prefix.end(), target) - cut_prefix.begin();
+        const uint32_t v = i < cuts.size() ? cuts[i] : n;
         b[k] = std::min(n, std::max(b[k - 1], v));
     }
     return b;

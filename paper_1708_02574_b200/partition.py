@@ -26,19 +26,51 @@ from .tpa import CpiParams, CpiResult, SeedSet, _terminal
 COMM_ID_BYTES = 128
 
 
+# SpMV tiling constants (csrc/cpi_kernels.cuh kMvTileNnz / kMvTileRows)
+TILE_NNZ, TILE_ROWS = 2048, 512
+
+
+def item_starts(rp: np.ndarray, n: int) -> list:
+    """Rows where the whole graph's SpMV tiling (tpa_gpu.cu build_items)
+    starts an item: greedy tiles of <= TILE_ROWS rows / TILE_NNZ nnz, rows
+    longer than TILE_NNZ alone."""
+    starts, r = [], 0
+    while r < n:
+        if rp[r + 1] - rp[r] > TILE_NNZ:
+            starts.append(r)
+            r += 1
+            continue
+        start, nnz = r, 0
+        while r < n and r - start < TILE_ROWS:
+            L = rp[r + 1] - rp[r]
+            if L > TILE_NNZ or (r > start and nnz + L > TILE_NNZ):
+                break
+            nnz += L
+            r += 1
+            if nnz >= TILE_NNZ:
+                break
+        starts.append(start)
+    return starts
+
+
 def partition_rows(indeg: np.ndarray, nranks: int) -> np.ndarray:
-    """Row boundaries balanced by nnz (tpa_part.cuh partition_rows): boundary k
-    is the first row whose in-degree prefix reaches floor(m*k/G)."""
+    """Row boundaries of the library's partitions (tpa_part.cuh partition_rows):
+    nnz-balanced, cut only at item starts of the whole graph's tiling, boundary
+    k the first cut whose in-degree prefix reaches floor(m*k/G)."""
     indeg = np.asarray(indeg, dtype=np.uint64)
     n = indeg.size
     prefix = np.zeros(n + 1, np.uint64)
     np.cumsum(indeg, out=prefix[1:])
     m = int(prefix[-1])
+    rp = prefix.astype(np.int64)
+    cuts = np.array(sorted(item_starts(rp, n) + [n]), np.int64)
+    cut_prefix = prefix[cuts]
     b = np.zeros(nranks + 1, np.int64)
     b[nranks] = n
     for k in range(1, nranks):
         target = (m * k) // nranks
-        v = int(np.searchsorted(prefix, np.uint64(target), side="left"))
+        i = int(np.searchsorted(cut_prefix, np.uint64(target), side="left"))
+        v = int(cuts[i]) if i < cuts.size else n
         b[k] = min(n, max(int(b[k - 1]), v))
     return b
 

@@ -23,25 +23,28 @@ C, EPS, T = 0.15, 1e-9, 10
 
 
 def test_partition_rows_balanced_and_covering():
+    from paper_1708_02574_b200.partition import TILE_NNZ, item_starts
     g = P.generate_rmat(12, 16, rng_seed=3)
     indeg = in_degrees(g)
     m = int(indeg.sum())
+    prefix = np.concatenate([[0], np.cumsum(indeg)]).astype(np.int64)
+    cuts = set(item_starts(prefix, g.node_count())) | {g.node_count()}
     for G in (1, 2, 3, 4, 8, 64):
         b = partition_rows(indeg, G)
         assert b[0] == 0 and b[-1] == g.node_count() and np.all(np.diff(b) >= 0)
-        prefix = np.concatenate([[0], np.cumsum(indeg)])
-        # each boundary is the first row reaching its share of the nnz
         for k in range(1, G):
+            assert int(b[k]) in cuts  # cut at a tile start only
             assert prefix[b[k]] >= (m * k) // G
-            assert b[k] == 0 or prefix[b[k] - 1] < (m * k) // G or b[k] == b[k - 1]
         nnz = np.diff(prefix[b])
-        assert nnz.max() <= m / G + indeg.max()
+        assert nnz.max() <= m / G + TILE_NNZ + indeg.max()
 
 
 def test_partition_rows_degenerate():
     assert list(partition_rows([0, 0, 0], 2)) == [0, 0, 3]
     assert list(partition_rows([5], 4)) == [0, 1, 1, 1, 1]
-    assert list(partition_rows([1, 2, 3, 0, 4, 5], 3)) == [0, 3, 5, 6]
+    # one 2048-nnz tile holds all six rows: no interior cut
+    assert list(partition_rows([1, 2, 3, 0, 4, 5], 3)) == [0, 6, 6, 6]
+    assert list(partition_rows([3000, 1, 3000, 1], 2)) == [0, 2, 4]
 
 
 def _free_port():
