@@ -350,6 +350,9 @@ def run_ours(args):
     dg.profile(True)
     if pg is not None:
         N.check(lib.tpa_graph_profile(pg.h, 1))
+    prof_range = os.environ.get("TPA_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
@@ -362,6 +365,8 @@ def run_ours(args):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             lib.tpa_artifact_destroy(a)
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     launches = dg.launches() + (N.lib.tpa_graph_launches(pg.h) if pg is not None else 0) - launches0
     mv_cnt, mv_ms = dg.profile_read(1)
     if pg is not None:
