@@ -41,8 +41,14 @@ constexpr int kThreads = 256;         // CTA size of every step kernel
 constexpr int kGroupItems = 128;      // items per first-level ticket group
 
 // SpMV (B = 1) tiling.
-constexpr int kMvTileNnz = 2048;      // gathered values staged in smem per CTA
-constexpr int kMvTileRows = 512;
+#ifndef TPA_MV_TILE
+#define TPA_MV_TILE 2048
+#endif
+#ifndef TPA_MV_ROWS
+#define TPA_MV_ROWS 512
+#endif
+constexpr int kMvTileNnz = TPA_MV_TILE;  // gathered values staged in smem per CTA
+constexpr int kMvTileRows = TPA_MV_ROWS;
 constexpr int kMvShortRow = 32;       // rows <= this: one thread, sequential
 
 // Per-column CPI state, double-buffered by sweep parity.

@@ -55,7 +55,11 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
     return s;
 }
 
+#ifdef TPA_MV2_MINB  // A/B knob; the default (no minimum) compiles to 40 registers, 6 CTAs/SM
+__global__ void __launch_bounds__(kThreads, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
+#else
 __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
+#endif
     const StepArgs& a = M.s;
     __shared__ double s_vals[kMvTileNnz];
     __shared__ int64_t s_rp[kMvTileRows + 1];

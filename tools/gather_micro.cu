@@ -94,6 +94,55 @@ __global__ void gather_bulk(const double* __restrict__ X, const uint32_t* __rest
     if (s == 12345.678) out[0] = s;
 }
 
+
+// C: cp.async 16 B per lane into a per-warp ring of S stages x R rows; lane
+// pair (2 rows per instruction: lanes 0-15 row a, 16-31 row b), consumer reads
+// lane = column (8 B) per row.
+template <int S, int R>
+__global__ void gather_ldgsts(const double* __restrict__ X, const uint32_t* __restrict__ idx, long long m, double* out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem) + (size_t)w * S * R * B;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = ((m + nw - 1) / nw + R - 1) / R * R;
+    const long long lo = warp * per, hi = min(m, lo + per);
+    const long long nst = (hi > lo) ? (hi - lo + R - 1) / R : 0;
+    const int half = lane >> 4, q = lane & 15;  // row within pair, 16-byte chunk
+    auto issue = [&](long long k) {
+        if (k < nst) {
+            const int slot = (int)(k % S);
+            const long long e0 = lo + k * R;
+            // indices for this stage: lane j < R holds idx[e0 + j]
+            const uint32_t myidx = (lane < R && e0 + lane < hi) ? __ldg(idx + e0 + lane) : 0u;
+#pragma unroll
+            for (int p = 0; p < R / 2; ++p) {
+                const int j = 2 * p + half;
+                const uint32_t u = __shfl_sync(0xffffffffu, myidx, j);
+                if (e0 + j < hi) {
+                    const double* src = X + (size_t)u * B + q * 2;
+                    const uint32_t d = (uint32_t)__cvta_generic_to_shared(ring + ((size_t)slot * R + j) * B + q * 2);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) issue(k);
+    double s = 0.0;
+    for (long long k = 0; k < nst; ++k) {
+        issue(k + S - 1);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1) : "memory");
+        __syncwarp();
+        const int slot = (int)(k % S);
+        const int cnt = (int)min((long long)R, hi - (lo + k * R));
+        for (int j = 0; j < cnt; ++j) s += ring[((size_t)slot * R + j) * B + lane];
+        __syncwarp();
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
 int main(int argc, char** argv) {
     const uint32_t n = 1 << 20;
     const long long m = 16586831;
@@ -134,6 +183,22 @@ int main(int argc, char** argv) {
         snprintf(nm, 64, "LDG U=16, %d warps/SM", warps);
         timeit(nm, [&] { gather_ldg<16><<<sms * warps / 8, 256>>>(X, idx, m, out); });
     }
+    auto ring = [&](auto kern, int S, int R, int wpb) {
+        const size_t smem = (size_t)wpb * S * R * B * 8;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem);
+        char nm[80];
+        snprintf(nm, 80, "LDGSTS S=%d R=%d %dw x %d CTA/SM", S, R, wpb, occ);
+        timeit(nm, [&] { kern<<<sms * occ, wpb * 32, smem>>>(X, idx, m, out); });
+    };
+    ring(gather_ldgsts<3, 16>, 3, 16, 4);
+    ring(gather_ldgsts<4, 16>, 4, 16, 4);
+    ring(gather_ldgsts<3, 8>, 3, 8, 4);
+    ring(gather_ldgsts<4, 8>, 4, 8, 4);
+    ring(gather_ldgsts<6, 8>, 6, 8, 4);
+    ring(gather_ldgsts<8, 8>, 8, 8, 2);
+    ring(gather_ldgsts<3, 32>, 3, 32, 2);
     for (int S : {2, 4}) {
         for (int wpb : {4, 8}) {
             const size_t smem = (size_t)wpb * S * 32 * B * 8 + wpb * S * 8;
