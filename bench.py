@@ -471,6 +471,42 @@ def run_ours(args):
                "note": "C-ABI with host buffers: seeds from host, stranger + every full score vector "
                        "copied back to pinned host memory (the reference API returns ScoreVectors)"}
 
+    # the CLI's query output (rwrank_main.cpp:158-165, --top-k 10): device top-k,
+    # only B*k ids + scores cross PCIe
+    e2e_topk = None
+    if not args.no_e2e:
+        K = 10
+        ids_h = torch.empty((batch, K), dtype=torch.int32, pin_memory=True)
+        vals_h = torch.empty((batch, K), dtype=torch.float64, pin_memory=True)
+        el = []
+        for it in range(1 + max(1, min(args.steps, args.e2e_steps))):  # first one: untimed warm-up
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            art = C_.c_void_p()
+            if pg is None:
+                N.check(lib.tpa_preprocess(h, C, EPS, T, None, C_.byref(art), 0))
+            else:
+                N.check(lib.tpa_preprocess(pg.h, C, EPS, T, d_str.data_ptr(), None, N.TPA_DEVICE_PTRS))
+                N.check(lib.tpa_artifact_create(h, d_str.data_ptr(), g.fingerprint(), C, EPS, T, N.TPA_DEVICE_PTRS,
+                                                C_.byref(art)))
+            for b in batches:
+                N.check(lib.tpa_query_batch_topk(h, art, b.ctypes.data, len(b), S, K, ids_h.data_ptr(),
+                                                 vals_h.data_ptr(), 0))
+            torch.cuda.synchronize()
+            if it:
+                el.append(time.perf_counter() - t0)
+            lib.tpa_artifact_destroy(art)
+        tt = torch.tensor([sum(el)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_topk = {"value": edges_per_step * jobs * len(el) / float(tt.item()) / 1e9, "unit": "GTEPS",
+                    "k": K, "h2d_bytes_per_step": len(seeds) * 4, "d2h_bytes_per_step": len(seeds) * K * 12,
+                    "queries_per_s": nq * jobs * len(el) / float(tt.item()),
+                    "ms_per_step": float(tt.item()) / len(el) * 1e3,
+                    "note": "tpa_query_batch_topk: query batch + device top_k_nodes (metrics.cpp:25-36); "
+                            "ids and scores of the top 10 per seed to pinned host memory"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_measure(g, seeds, cfg_name, budget_s=args.cpu_budget)
@@ -483,7 +519,7 @@ def run_ours(args):
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg_name, g, nq, batch),
             "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_topk": e2e_topk, "gpu_launches": launches,
             "clocks": clk.summary(), "ingest_s": t_ingest, "graph_build_s": t_build,
             "parallelism": (f"row-partitioned preprocess (NCCL all-reduce + all-gather per sweep) + "
                             f"queries split over {world} whole-graph replicas" if partitioned else

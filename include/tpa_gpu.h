@@ -153,6 +153,20 @@ int tpa_query_batch(tpa_graph *g, const tpa_artifact *a, const uint32_t *seeds, 
 int tpa_query_na_batch(tpa_graph *g, const uint32_t *seeds, uint32_t B, uint32_t S, uint32_t T,
                        double c, double eps, double *out, int flags);
 
+/* --- top-k on the device --------------------------------
+ * Replaces: top_k_nodes(scores, k) (metrics.hpp:17, metrics.cpp:25-36) for B
+ * vectors: score descending, equal scores by ascending node id; k in [1, n]
+ * else TPA_ERR_OUT_OF_RANGE ("k must be in [1, n], got k").  scores: [B][n]
+ * (what tpa_query_batch writes); out_ids / out_scores: [B][k] (out_scores may
+ * be NULL).  All arrays host, or device with TPA_DEVICE_PTRS. */
+int tpa_top_k(tpa_graph *g, const double *scores, uint32_t B, uint32_t k, uint32_t *out_ids,
+              double *out_scores, int flags);
+/* tpa_query_batch (or, with TPA_QUERY_NA, the artifact-free query_na using the
+ * artifact's c / eps / T) followed by tpa_top_k on the device: only B*k results
+ * leave the GPU (the CLI's query output, rwrank_main.cpp:158-165). */
+int tpa_query_batch_topk(tpa_graph *g, const tpa_artifact *a, const uint32_t *seeds, uint32_t B,
+                         uint32_t S, uint32_t k, uint32_t *out_ids, double *out_scores, int flags);
+
 /* --- multi-GPU: row-partitioned CPI (B = 1) ---------------------------------
  * The north star's multi-GPU layout: the rows of CSR(Ãᵀ) are split into
  * nnz-balanced ranges, one per GPU; each sweep is the single-GPU kernel on

@@ -10,13 +10,13 @@ from .graph import (DanglingPolicy, DeviceGraph, Graph, dangling_policy_from_str
 from .partition import PartitionedGraph, PartitionGroup, partition_rows
 from .tpa import (CpiParams, CpiResult, SeedSet, StrangerArtifact, TpaParams, cpi_partition, cpi_run,
                   exact_rwr, exact_rwr_batch, kDefaultRestartProb, kDefaultTolerance, neighbor_scale_factor,
-                  pagerank, preprocess, query, query_batch, query_na)
+                  pagerank, preprocess, query, query_batch, query_batch_topk, query_na, top_k)
 
 __all__ = [
     "CudaError", "DanglingPolicy", "DeviceGraph", "Graph", "dangling_policy_from_string", "fingerprint",
     "generate_random_graph", "generate_rmat", "propagation_sweep", "sample_seeds", "to_string",
     "CpiParams", "CpiResult", "SeedSet", "StrangerArtifact", "TpaParams", "cpi_partition", "cpi_run",
     "exact_rwr", "exact_rwr_batch", "kDefaultRestartProb", "kDefaultTolerance", "neighbor_scale_factor",
-    "pagerank", "preprocess", "query", "query_batch", "query_na",
+    "pagerank", "preprocess", "query", "query_batch", "query_na", "query_batch_topk", "top_k",
     "PartitionedGraph", "PartitionGroup", "partition_rows",
 ]

@@ -51,6 +51,8 @@ SIGNATURES = {
     "tpa_query": ([_vp, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_query_batch": ([_vp, _vp, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_query_na_batch": ([_vp, _vp, _u32, _u32, _u32, _dbl, _dbl, _vp, _int], _int),
+    "tpa_top_k": ([_vp, _vp, _u32, _u32, _vp, _vp, _int], _int),
+    "tpa_query_batch_topk": ([_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _int], _int),
     "tpa_comm_unique_id": ([_vp], _int),
     "tpa_graph_create_part": ([_u32, _u64, _vp, _vp, _int, _u64, _int, _u32, _u32, _vp, C.POINTER(_vp)], _int),
     "tpa_graph_part_info": ([_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32),

@@ -495,6 +495,9 @@ struct tpa_graph {
     DevBuf out_stage;  // host-output staging for batch calls
     std::set<tpa_artifact*> artifacts;  // detached (buffers freed) on destroy
     std::unique_ptr<PartInfo> part;     // row partition (multi-GPU), or null: whole graph
+    struct TopkWork {
+        DevBuf st, hist, cand, ids;  // device top-k (tpa_topk.cuh): state, histograms, candidates, picks
+    } topk;
     uint64_t launches = 0;
     int num_sms = 148;
     std::mutex mu;
@@ -1281,6 +1284,7 @@ int tpa_graph_destroy(tpa_graph* g) {
                               &g->longs.win_blk_w[3]})
                 d->release();
             g->init_part.release();
+            for (DevBuf* d : {&g->topk.st, &g->topk.hist, &g->topk.cand, &g->topk.ids}) d->release();
             g->out_stage.release();
             for (tpa_artifact* a : g->artifacts) detach_artifact(a);
             g->artifacts.clear();
@@ -1692,3 +1696,4 @@ int tpa_query_na_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, uint32_t
 }  // extern "C"
 
 #include "tpa_part.cuh"
+#include "tpa_topk.cuh"

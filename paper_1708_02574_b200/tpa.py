@@ -295,3 +295,56 @@ def query_batch(g: Graph, artifact: StrangerArtifact, seeds, family_end: int, ou
             (N.TPA_QUERY_NA if na else 0) | (N.TPA_ASYNC if (odev and not sync) else 0)
     check(lib.tpa_query_batch(dg.h, artifact.device(g), sp, B, int(family_end), p, flags))
     return out
+
+
+def _seed_array(seeds, n):
+    if type(seeds).__module__.startswith("torch"):
+        seeds = seeds.detach().cpu().numpy()
+    s = np.ascontiguousarray(np.asarray(seeds).astype(np.int64, copy=False))
+    if s.size and (s.min() < 0 or s.max() > 0xFFFFFFFF):
+        bad = int(s[(s < 0) | (s > 0xFFFFFFFF)][0])
+        raise IndexError(f"seed id {bad} out of range for graph with {n} nodes")
+    return np.ascontiguousarray(s, np.uint32)
+
+
+def top_k(g: Graph, scores, k: int):
+    """metrics.hpp:17 / metrics.cpp:25-36 ``top_k_nodes`` for one vector [n] or
+    B vectors [B][n] on the GPU: (ids [B][k] uint32, scores [B][k]), score
+    descending, ties by ascending id.  ``scores``: numpy or torch (CUDA
+    tensors stay on the device and the results come back as CUDA tensors)."""
+    n = g.node_count()
+    if k < 1 or k > n:
+        raise IndexError(f"k must be in [1, n], got {k}")
+    dg = _dev(g)
+    single = getattr(scores, "ndim", 2) == 1
+    is_torch = type(scores).__module__.startswith("torch")
+    if is_torch and scores.is_cuda:
+        import torch
+        sc = scores.contiguous().view(-1, n).to(torch.float64)
+        B = sc.shape[0]
+        ids = torch.empty((B, k), dtype=torch.int32, device=sc.device)
+        vals = torch.empty((B, k), dtype=torch.float64, device=sc.device)
+        check(lib.tpa_top_k(dg.h, sc.data_ptr(), B, int(k), ids.data_ptr(), vals.data_ptr(), N.TPA_DEVICE_PTRS))
+        return (ids[0], vals[0]) if single else (ids, vals)
+    sc = np.ascontiguousarray(np.asarray(scores.cpu() if is_torch else scores, np.float64)).reshape(-1, n)
+    B = sc.shape[0]
+    ids = np.empty((B, k), np.uint32)
+    vals = np.empty((B, k), np.float64)
+    check(lib.tpa_top_k(dg.h, sc.ctypes.data, B, int(k), ids.ctypes.data, vals.ctypes.data, 0))
+    return (ids[0], vals[0]) if single else (ids, vals)
+
+
+def query_batch_topk(g: Graph, artifact: StrangerArtifact, seeds, family_end: int, k: int, na: bool = False):
+    """``query_batch`` + ``top_k_nodes`` per seed on the device (the CLI's query
+    output, rwrank_main.cpp:158-165): only B·k ids / scores reach the host."""
+    _check_artifact(g, artifact, family_end)
+    n = g.node_count()
+    if k < 1 or k > n:
+        raise IndexError(f"k must be in [1, n], got {k}")
+    s = _seed_array(seeds, n)
+    B = int(s.size)
+    ids = np.empty((B, k), np.uint32)
+    vals = np.empty((B, k), np.float64)
+    check(lib.tpa_query_batch_topk(_dev(g).h, artifact.device(g), s.ctypes.data, B, int(family_end), int(k),
+                                   ids.ctypes.data, vals.ctypes.data, N.TPA_QUERY_NA if na else 0))
+    return ids, vals
