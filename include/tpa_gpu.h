@@ -224,6 +224,12 @@ int tpa_host_graph_from_edges(uint32_t n, const uint32_t *src, const uint32_t *d
  * dropped, duplicates removed by the construction. */
 int tpa_host_graph_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
                         uint64_t seed, int policy, int threads, tpa_host_graph **out);
+/* The same construction on the GPU: sort + dedupe, dangling
+ * list, SelfLoop repair and out-CSR on `device`, FNV-1a on the host; the
+ * result is identical to tpa_host_graph_from_edges.  Errors as the reference
+ * constructor (first out-of-range edge in input order -> TPA_ERR_OUT_OF_RANGE). */
+int tpa_host_graph_build_gpu(uint32_t n, const uint32_t *src, const uint32_t *dst, uint64_t m,
+                             int policy, int device, tpa_host_graph **out);
 /* generate_random_graph(n, m, seed, policy) semantics (graph.cpp:166-205). */
 int tpa_host_graph_random(uint32_t n, uint64_t m, uint64_t seed, int policy,
                           tpa_host_graph **out);

@@ -71,6 +71,22 @@ uint64_t fingerprint_of(uint32_t n, uint64_t m, const uint64_t* off, const uint3
     return f.h;
 }
 
+}  // namespace
+
+tpa_host_graph* tpa::make_host_graph(uint32_t n, int policy, std::vector<uint64_t>&& off,
+                                     std::vector<uint32_t>&& tgt, std::vector<uint32_t>&& dangling) {
+    auto* g = new tpa_host_graph;
+    g->n = n;
+    g->policy = policy;
+    g->off = std::move(off);
+    g->tgt = std::move(tgt);
+    g->dangling = std::move(dangling);
+    g->fingerprint = fingerprint_of(n, g->tgt.size(), g->off.data(), g->tgt.data(), policy);
+    return g;
+}
+
+namespace {
+
 // graph.cpp:53-91 semantics: validate, sort + dedupe per source, dangling
 // list before the policy, SelfLoop repair edge, out-CSR, fingerprint.
 tpa_host_graph* build(uint32_t n, const uint32_t* src, const uint32_t* dst, uint64_t m,

@@ -1697,3 +1697,4 @@ int tpa_query_na_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, uint32_t
 
 #include "tpa_part.cuh"
 #include "tpa_topk.cuh"
+#include "tpa_graph_build.cuh"

@@ -3,9 +3,11 @@
 // thread-local error message behind tpa_last_error().
 #pragma once
 
+#include <cstdint>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "tpa_gpu.h"
 
@@ -20,6 +22,11 @@ struct alloc_error : std::runtime_error {
 };
 
 std::string& last_error();
+
+// A host graph (tpa_host_graph) from its finished out-CSR and dangling list;
+// computes the FNV-1a fingerprint (graph.cpp:84-90).  host_graph.cpp.
+tpa_host_graph* make_host_graph(uint32_t n, int policy, std::vector<uint64_t>&& off, std::vector<uint32_t>&& tgt,
+                                std::vector<uint32_t>&& dangling);
 
 template <class F>
 int guard(F&& f) {

@@ -60,6 +60,19 @@ class Graph:
         self._adopt(h)
 
     @classmethod
+    def build_gpu(cls, node_count: int, edges, policy=DanglingPolicy.SelfLoop, device: int = 0) -> "Graph":
+        """The constructor's work (graph.cpp:53-91) on the GPU (sort, dedupe,
+        dangling list, SelfLoop repair, out-CSR); FNV-1a on the host.  Same
+        result and errors as ``Graph(node_count, edges, policy)``."""
+        src, dst = _edge_arrays(edges)
+        if node_count < 0 or node_count > 0xFFFFFFFF:
+            raise ValueError("node_count out of uint32 range")
+        h = C.c_void_p()
+        check(lib.tpa_host_graph_build_gpu(int(node_count), src.ctypes.data, dst.ctypes.data, len(src),
+                                           int(_policy(policy)), int(device), C.byref(h)))
+        return cls._from_handle(h)
+
+    @classmethod
     def _from_handle(cls, h) -> "Graph":
         g = cls.__new__(cls)
         g._adopt(h)
