@@ -153,6 +153,22 @@ int tpa_query_batch(tpa_graph *g, const tpa_artifact *a, const uint32_t *seeds, 
 int tpa_query_na_batch(tpa_graph *g, const uint32_t *seeds, uint32_t B, uint32_t S, uint32_t T,
                        double c, double eps, double *out, int flags);
 
+/* --- artifact I/O from device buffers -------------------
+ * Replaces: save_artifact / load_artifact (persistence.hpp, persistence.cpp:
+ * 69-125), the file format unchanged (48 + 8n bytes, CRC-32 trailer); the
+ * CRC-32 runs on the GPU.  Errors: the reference's std::runtime_error texts
+ * (TPA_ERR_RUNTIME), checked in the reference's order.  A loaded artifact is
+ * bound to graph g (its fingerprint is checked by the queries, tpa.cpp:63-64). */
+int tpa_artifact_save(const tpa_artifact *a, const char *path);
+int tpa_artifact_load(tpa_graph *g, const char *path, tpa_artifact **out);
+int tpa_artifact_info(const tpa_artifact *a, uint64_t *n, double *c, double *eps, uint32_t *T,
+                      uint64_t *fingerprint);
+/* the stranger scores (n doubles; host, or device with TPA_DEVICE_PTRS) */
+int tpa_artifact_scores(const tpa_artifact *a, double *out, int flags);
+/* CRC-32 (persistence.cpp:16-32) of `size` bytes on the GPU (data host, or
+ * device with TPA_DEVICE_PTRS). */
+int tpa_crc32(const void *data, uint64_t size, int flags, int device, uint32_t *out);
+
 /* --- top-k on the device --------------------------------
  * Replaces: top_k_nodes(scores, k) (metrics.hpp:17, metrics.cpp:25-36) for B
  * vectors: score descending, equal scores by ascending node id; k in [1, n]

@@ -10,7 +10,8 @@ from .graph import (DanglingPolicy, DeviceGraph, Graph, dangling_policy_from_str
 from .partition import PartitionedGraph, PartitionGroup, partition_rows
 from .tpa import (CpiParams, CpiResult, SeedSet, StrangerArtifact, TpaParams, cpi_partition, cpi_run,
                   exact_rwr, exact_rwr_batch, kDefaultRestartProb, kDefaultTolerance, neighbor_scale_factor,
-                  pagerank, preprocess, query, query_batch, query_batch_topk, query_na, top_k)
+                  pagerank, preprocess, query, query_batch, query_batch_topk, query_na, top_k,
+                  save_artifact, load_artifact, crc32)
 
 __all__ = [
     "CudaError", "DanglingPolicy", "DeviceGraph", "Graph", "dangling_policy_from_string", "fingerprint",
@@ -18,5 +19,6 @@ __all__ = [
     "CpiParams", "CpiResult", "SeedSet", "StrangerArtifact", "TpaParams", "cpi_partition", "cpi_run",
     "exact_rwr", "exact_rwr_batch", "kDefaultRestartProb", "kDefaultTolerance", "neighbor_scale_factor",
     "pagerank", "preprocess", "query", "query_batch", "query_na", "query_batch_topk", "top_k",
+    "save_artifact", "load_artifact", "crc32",
     "PartitionedGraph", "PartitionGroup", "partition_rows",
 ]

@@ -51,6 +51,12 @@ SIGNATURES = {
     "tpa_query": ([_vp, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_query_batch": ([_vp, _vp, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_query_na_batch": ([_vp, _vp, _u32, _u32, _u32, _dbl, _dbl, _vp, _int], _int),
+    "tpa_artifact_save": ([_vp, C.c_char_p], _int),
+    "tpa_artifact_load": ([_vp, C.c_char_p, C.POINTER(_vp)], _int),
+    "tpa_artifact_info": ([_vp, C.POINTER(_u64), C.POINTER(_dbl), C.POINTER(_dbl), C.POINTER(_u32),
+                           C.POINTER(_u64)], _int),
+    "tpa_artifact_scores": ([_vp, _vp, _int], _int),
+    "tpa_crc32": ([_vp, _u64, _int, _int, C.POINTER(_u32)], _int),
     "tpa_top_k": ([_vp, _vp, _u32, _u32, _vp, _vp, _int], _int),
     "tpa_query_batch_topk": ([_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _int], _int),
     "tpa_comm_unique_id": ([_vp], _int),

@@ -607,6 +607,7 @@ struct tpa_graph {
 struct tpa_artifact {
     tpa_graph* g = nullptr;  // null once the graph is gone (buffers freed then)
     DevBuf stranger;
+    uint64_t n = 0;  // entries of `stranger`
     uint64_t fingerprint = 0;
     double c = 0.15, eps = 1e-9;
     uint32_t T = 10;
@@ -1575,6 +1576,7 @@ int tpa_preprocess(tpa_graph* g, double c, double eps, uint32_t T, double* out_s
         art->c = c;
         art->eps = eps;
         art->T = T;
+        art->n = g->n;
         art->stranger.ensure((size_t)g->n * 8, g->stream);
         RunCfg cfg;
         cfg.B = 1;
@@ -1614,6 +1616,7 @@ int tpa_artifact_create(tpa_graph* g, const double* stranger, uint64_t graph_fin
         art->c = c;
         art->eps = eps;
         art->T = T;
+        art->n = g->n;
         art->stranger.ensure((size_t)g->n * 8, g->stream);
         CK(cudaMemcpyAsync(art->stranger.p, stranger, (size_t)g->n * 8,
                            (flags & TPA_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
@@ -1642,6 +1645,7 @@ static void check_query(tpa_graph* g, const tpa_artifact* a, uint32_t S) {
     // tpa.cpp:63-66, then cpi_run's CpiParams::validate with the artifact's c/eps (tpa.cpp:69)
     if (a->fingerprint != g->fingerprint)
         throw std::runtime_error("stale artifact: graph fingerprint mismatch");
+    if (a->n != g->n) throw std::runtime_error("stale artifact: graph fingerprint mismatch");
     if (a->g == nullptr) throw std::runtime_error("artifact outlived its graph handle");
     if (a->g->device != g->device) throw std::invalid_argument("artifact lives on another device");
     if (S < 1 || S >= a->T) throw std::invalid_argument("family_end (S) must satisfy 1 <= S < T");
@@ -1698,3 +1702,4 @@ int tpa_query_na_batch(tpa_graph* g, const uint32_t* seeds, uint32_t B, uint32_t
 #include "tpa_part.cuh"
 #include "tpa_topk.cuh"
 #include "tpa_graph_build.cuh"
+#include "tpa_artifact_io.cuh"

@@ -348,3 +348,35 @@ def query_batch_topk(g: Graph, artifact: StrangerArtifact, seeds, family_end: in
     check(lib.tpa_query_batch_topk(_dev(g).h, artifact.device(g), s.ctypes.data, B, int(family_end), int(k),
                                    ids.ctypes.data, vals.ctypes.data, N.TPA_QUERY_NA if na else 0))
     return ids, vals
+
+
+def save_artifact(artifact: StrangerArtifact, path, g: Graph) -> None:
+    """persistence.hpp save_artifact: the TPA1 file (48 + 8n bytes), written
+    from the artifact's device copy on g's GPU, CRC-32 computed on the GPU."""
+    check(lib.tpa_artifact_save(artifact.device(g), str(path).encode()))
+
+
+def load_artifact(path, g: Graph) -> StrangerArtifact:
+    """persistence.hpp load_artifact (same checks, same order, same messages;
+    RuntimeError), CRC-32 on the GPU; the artifact arrives bound to g's GPU."""
+    h = C.c_void_p()
+    check(lib.tpa_artifact_load(_dev(g).h, str(path).encode(), C.byref(h)))
+    n, c, eps, T, fp = C.c_uint64(), C.c_double(), C.c_double(), C.c_uint32(), C.c_uint64()
+    check(lib.tpa_artifact_info(h, C.byref(n), C.byref(c), C.byref(eps), C.byref(T), C.byref(fp)))
+    scores = np.empty(n.value, np.float64)
+    if n.value:
+        check(lib.tpa_artifact_scores(h, scores.ctypes.data, 0))
+    art = StrangerArtifact(scores, fp.value, c.value, eps.value, T.value)
+    if n.value == g.node_count():
+        art._dev = (_dev(g), art._key(), h)
+    else:
+        lib.tpa_artifact_destroy(h)
+    return art
+
+
+def crc32(data, device: int = 0) -> int:
+    """CRC-32 of a bytes-like object on the GPU (persistence.cpp:16-32)."""
+    buf = np.frombuffer(bytes(data), np.uint8)
+    out = C.c_uint32()
+    check(lib.tpa_crc32(buf.ctypes.data if buf.size else None, buf.size, 0, int(device), C.byref(out)))
+    return out.value
