@@ -55,7 +55,8 @@ enum tpa_policy { TPA_SELFLOOP = 0, TPA_UNIFORM = 1, TPA_DROP = 2 };
 
 enum tpa_flags {
     TPA_DEVICE_PTRS = 1,  /* vector in/out arguments are device pointers */
-    TPA_ASYNC = 2,        /* with TPA_DEVICE_PTRS: do not synchronise on return */
+    TPA_ASYNC = 2,        /* do not synchronise on return (device outputs; batch calls' host
+                             outputs drain asynchronously: tpa_graph_sync before reading) */
     TPA_NODE_MAJOR = 4,   /* batch output laid out [n][B] instead of [B][n] */
     TPA_QUERY_NA = 8      /* query_batch: no stranger term (tpa.cpp:78-86) */
 };
@@ -79,6 +80,10 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t *out_offsets,
                      tpa_graph **out);
 int tpa_graph_destroy(tpa_graph *g);
 /* Make the handle enqueue on an external cudaStream_t (NULL: its own stream). */
+/* Waits for every call enqueued on the handle (TPA_ASYNC), including the
+ * device-to-host drains of batch calls with host outputs: those compute chunk
+ * k+1 while chunk k drains over PCIe (two device staging buffers). */
+int tpa_graph_sync(tpa_graph *g);
 int tpa_graph_set_stream(tpa_graph *g, void *cuda_stream);
 int tpa_graph_info(const tpa_graph *g, uint32_t *n, uint64_t *m, uint64_t *fingerprint,
                    int *policy, uint64_t *device_bytes);

@@ -33,6 +33,7 @@ SIGNATURES = {
     "tpa_graph_create": ([_u32, _u64, _vp, _vp, _int, _u64, _int, C.POINTER(_vp)], _int),
     "tpa_graph_destroy": ([_vp], _int),
     "tpa_graph_set_stream": ([_vp, _vp], _int),
+    "tpa_graph_sync": ([_vp], _int),
     "tpa_graph_info": ([_vp, C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_int),
                         C.POINTER(_u64)], _int),
     "tpa_graph_launches": ([_vp], _u64),

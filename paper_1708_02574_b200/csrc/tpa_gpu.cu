@@ -492,7 +492,16 @@ struct tpa_graph {
     uint32_t n_blocks = 0;  // kMmRows-row blocks
     std::map<int, std::unique_ptr<Workspace>> ws;
     DevBuf init_part;
-    DevBuf out_stage;  // host-output staging for batch calls
+    DevBuf out_stage;  // (unused; kept for the handle layout of older callers)
+    // host-output pipeline of batch calls: chunk k computes into stage[k % 2] on
+    // `stream` while chunk k-1's results drain to the host on `copy`
+    struct HostPipe {
+        cudaStream_t copy = nullptr;
+        DevBuf stage[2];
+        cudaEvent_t done[2] = {nullptr, nullptr}, free_[2] = {nullptr, nullptr};
+        bool pending[2] = {false, false};
+        int slot = 0;
+    } pipe;
     std::set<tpa_artifact*> artifacts;  // detached (buffers freed) on destroy
     std::unique_ptr<PartInfo> part;     // row partition (multi-GPU), or null: whole graph
     struct TopkWork {
@@ -1020,9 +1029,23 @@ static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, d
         throw std::invalid_argument("node-major output needs B in {8, 16, 32, 64}");
     if (node_major && Btot == 1)
         throw std::invalid_argument("node-major output needs B in {8, 16, 32, 64}");
-    DevBuf& stage = g->out_stage;
-    if (!dev) stage.ensure((size_t)std::min<uint32_t>(Btot, 64) * n * sizeof(double), g->stream);
+    auto& P = g->pipe;
+    if (!dev && !P.copy) {
+        CK(cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaEventCreateWithFlags(&P.done[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&P.free_[k], cudaEventDisableTiming));
+        }
+    }
     for (uint32_t b0 = 0; b0 < Btot; b0 += 64) {
+        int slot = 0;
+        if (!dev) {
+            slot = P.slot;
+            P.slot ^= 1;
+            // the slot's previous drain must finish before it is overwritten (or reallocated)
+            if (P.pending[slot]) CK(cudaStreamWaitEvent(g->stream, P.free_[slot], 0));
+            P.stage[slot].ensure((size_t)std::min<uint32_t>(Btot, 64) * n * sizeof(double), g->stream);
+        }
         const uint32_t bv = std::min<uint32_t>(64, Btot - b0);
         const int B = batch_width(bv);
         Workspace& w = g->workspace(B);
@@ -1043,7 +1066,7 @@ static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, d
         }
         for (uint32_t b = 0; b < bv; ++b) cfg.seeds.s[b] = hseeds[b0 + b];
         cfg.acc = w.acc.as<double>();
-        double* dst = dev ? out + (node_major ? 0 : (size_t)b0 * n) : stage.as<double>();
+        double* dst = dev ? out + (node_major ? 0 : (size_t)b0 * n) : P.stage[slot].as<double>();
         if (combine) {
             cfg.out = dst;
             cfg.stranger = stranger;
@@ -1063,9 +1086,19 @@ static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, d
                 ++g->launches;
             }
         }
-        if (!dev) download(g, out + (size_t)b0 * n, stage.p, (size_t)bv * n * 8);
+        if (!dev) {
+            CK(cudaEventRecord(P.done[slot], g->stream));
+            CK(cudaStreamWaitEvent(P.copy, P.done[slot], 0));
+            CK(cudaMemcpyAsync(out + (size_t)b0 * n, P.stage[slot].p, (size_t)bv * n * 8, cudaMemcpyDeviceToHost,
+                               P.copy));
+            CK(cudaEventRecord(P.free_[slot], P.copy));
+            P.pending[slot] = true;
+        }
     }
-    finish(g, flags);
+    if (!(flags & TPA_ASYNC)) {
+        if (!dev) CK(cudaStreamSynchronize(P.copy));
+        CK(cudaStreamSynchronize(g->stream));
+    }
 }
 
 }  // namespace tpa
@@ -1287,6 +1320,14 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->init_part.release();
             for (DevBuf* d : {&g->topk.st, &g->topk.hist, &g->topk.cand, &g->topk.ids}) d->release();
             g->out_stage.release();
+            if (g->pipe.copy) {
+                cudaStreamSynchronize(g->pipe.copy);
+                for (int k = 0; k < 2; ++k) {
+                    g->pipe.stage[k].release();
+                    cudaEventDestroy(g->pipe.done[k]);
+                    cudaEventDestroy(g->pipe.free_[k]);
+                }
+            }
             for (tpa_artifact* a : g->artifacts) detach_artifact(a);
             g->artifacts.clear();
             cudaStreamSynchronize(g->stream);
@@ -1296,9 +1337,19 @@ int tpa_graph_destroy(tpa_graph* g) {
             }
             for (auto e : g->event_pool) cudaEventDestroy(e);
             if (g->own_stream) cudaStreamDestroy(g->stream);
+            if (g->pipe.copy) cudaStreamDestroy(g->pipe.copy);
             if (g->part) part_comm_destroy(g->part->comm);
         }
         delete g;
+    });
+}
+
+int tpa_graph_sync(tpa_graph* g) {
+    return guard([&] {
+        if (!g) throw std::invalid_argument("null graph");
+        DeviceGuard dg(g->device);
+        CK(cudaStreamSynchronize(g->stream));
+        if (g->pipe.copy) CK(cudaStreamSynchronize(g->pipe.copy));
     });
 }
 
