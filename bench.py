@@ -525,7 +525,7 @@ def run_ours(args):
             "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_topk": e2e_topk, "gpu_launches": launches,
             "clocks": clk.summary(), "ingest_s": t_ingest, "graph_build_s": t_build,
-            "parallelism": (f"row-partitioned preprocess (NCCL all-reduce + all-gather per sweep) + "
+            "parallelism": (f"row-partitioned preprocess (one NCCL all-gather per sweep: shares + exact residual limbs) + "
                             f"queries split over {world} whole-graph replicas" if partitioned else
                             f"independent replicas x{world}" if world > 1 else "single GPU"),
         }

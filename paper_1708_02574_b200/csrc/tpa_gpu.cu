@@ -462,12 +462,18 @@ struct LongRows {
 // nranks x slice doubles (row v of partition r at r*slice + v - bounds[r]),
 // so one in-place all-gather per sweep assembles the full share vector and
 // the column indices are stored pre-mapped to that layout.
+// After its S rows, every partition's span in the share buffer carries its
+// residual limbs (6 uint64 as doubles' bits), so one all-gather per sweep
+// moves the shares and the totals together.
+constexpr uint32_t kLimbPad = 8;
+
 struct PartInfo {
     uint32_t nranks = 1, rank = 0;
     uint32_t n_global = 0;
     uint64_t m_global = 0;
     std::vector<uint32_t> bounds;  // nranks + 1
-    uint32_t slice = 0;
+    uint32_t slice = 0;            // S: rows of the largest partition
+    uint32_t stride = 0;           // S + kLimbPad: a partition's span in the share layout
     ncclComm_t comm = nullptr;     // one rank per process; null: in-process group or nranks = 1
     uint32_t row_begin() const { return bounds[rank]; }
     uint32_t rows(uint32_t r) const { return bounds[r + 1] - bounds[r]; }
@@ -549,7 +555,7 @@ struct tpa_graph {
         // B > 1: one extra all-zero row (index n) that dead sources gather
         const size_t nb = (size_t)n * B * sizeof(double);
         // a partition's shares span the padded global layout (all partitions)
-        const size_t nbs = part ? (size_t)part->nranks * part->slice * sizeof(double)
+        const size_t nbs = part ? (size_t)part->nranks * part->stride * sizeof(double)
                                 : nb + (B > 1 ? (size_t)B * sizeof(double) : 0);
         if (w.share[0].bytes < nbs) {
             w.share[0].ensure(nbs, stream);
@@ -810,7 +816,9 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                 (void)carve;
                 k_step_spmv2<<<grid, block, 0, g->stream>>>(MvArgs{
                     a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
-                    g->part ? w.limbs.as<unsigned long long>() + (a.step & 1) * 6 : nullptr});
+                    !g->part ? nullptr
+                    : a.share_out ? reinterpret_cast<unsigned long long*>(a.share_out + g->part->slice)
+                                  : w.limbs.as<unsigned long long>() + (a.step & 1) * 6});
             }
             else
                 k_step_spmv<<<grid, block, 0, g->stream>>>(a);

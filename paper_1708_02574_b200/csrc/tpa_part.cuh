@@ -6,12 +6,14 @@
 //     (cpi_spmv2.cuh), reading the full share vector (padded global layout,
 //     PartInfo) and writing its own slice of the next one;
 //   * the residual / dangling totals are exact fixed-point integers, so the
-//     all-reduce of their limbs gives every partition the one-GPU totals bit
-//     for bit, and k_part_finalize advances the same ColState everywhere;
-//   * the share slices are all-gathered in place.
+//     sum of every partition's limbs gives the one-GPU totals bit for bit,
+//     and k_part_finalize advances the same ColState everywhere;
+//   * each partition's limbs ride at the end of its span of the share buffer,
+//     so ONE in-place all-gather per sweep moves shares and totals (a sweep
+//     without a next iterate -- the terminal one -- all-reduces the limbs).
 // Two transports with one driver (run_cpi_part):
-//   * one process per GPU: NCCL (ncclAllReduce of 6 uint64 + in-place
-//     ncclAllGather of the slice) on the partition's stream;
+//   * one process per GPU: NCCL (in-place ncclAllGather of the span) on the
+//     partition's stream;
 //   * one process driving all partitions (tpa_group): stream-ordered peer
 //     copies (cudaMemcpyPeerAsync) and a limb-sum kernel, no host sync.
 // Included at the end of tpa_gpu.cu.
@@ -77,7 +79,7 @@ __global__ void k_indeg(const uint32_t* __restrict__ tgt, uint64_t m, uint32_t* 
 }
 
 // Sort keys for partition [lo, hi): local row of in-range edges (others sort
-// last), value = the source's index in the padded share layout.
+// last), value = the source's index in the padded share layout (stride S).
 __global__ void k_part_keys(const uint32_t* __restrict__ tgt, const uint32_t* __restrict__ src, uint64_t m,
                             uint32_t lo, uint32_t hi, const uint32_t* __restrict__ bounds, uint32_t G,
                             uint32_t S, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
@@ -170,6 +172,7 @@ static void build_part(tpa_graph* g, uint32_t n, uint64_t m, const uint64_t* out
     uint32_t S = 1;
     for (uint32_t r = 0; r < nranks; ++r) S = std::max(S, P->rows(r));
     P->slice = S;
+    P->stride = S + kLimbPad;
     const uint32_t lo = P->bounds[rank], hi = P->bounds[rank + 1], nl = hi - lo;
     const uint64_t ml = prefix[hi] - prefix[lo];
 
@@ -183,7 +186,7 @@ static void build_part(tpa_graph* g, uint32_t n, uint64_t m, const uint64_t* out
     k_expand_src<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>(), n, d_src.as<uint32_t>());
     CKL("k_expand_src");
     k_part_keys<<<blocks, 256, 0, s>>>(d_tgt.as<uint32_t>(), d_src.as<uint32_t>(), m, lo, hi,
-                                       d_bounds.as<uint32_t>(), nranks, S, d_keys.as<uint32_t>(),
+                                       d_bounds.as<uint32_t>(), nranks, P->stride, d_keys.as<uint32_t>(),
                                        d_vals.as<uint32_t>());
     CKL("k_part_keys");
     if (m) {
@@ -226,20 +229,44 @@ struct PartRun {
 static unsigned long long* limbs_slot(Workspace& w, int slot) { return w.limbs.as<unsigned long long>() + slot * 6; }
 static unsigned long long* limbs_total(Workspace& w) { return w.limbs.as<unsigned long long>() + 18; }
 
-// All-reduce the limbs of `slot` into every partition's totals, then (share
-// >= 0) all-gather share buffer `share`.  Stream-ordered, no host sync.
+// The limbs a partition publishes for sweep `slot` (0/1 by parity, 2 = x⁰):
+// at the end of its span of share buffer `share` when the sweep writes one,
+// else in the workspace.
+static unsigned long long* limbs_at(tpa_graph* g, int slot, int share) {
+    Workspace& w = g->workspace(1);
+    const PartInfo& P = *g->part;
+    if (share < 0) return limbs_slot(w, slot);
+    return reinterpret_cast<unsigned long long*>(w.share[share].as<double>() + (size_t)P.rank * P.stride + P.slice);
+}
+
+// Every partition's totals for `slot`: with a share buffer, one in-place
+// all-gather of the spans (shares + limbs) and a local sum of the G limb
+// sets; without, an all-reduce of the limbs.  Stream-ordered, no host sync.
 static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share) {
     const uint32_t G = Pg[0]->part->nranks;
+    auto sum_local = [&](tpa_graph* g) {  // the G limb sets of g's gathered buffer
+        Workspace& w = g->workspace(1);
+        const PartInfo& P = *g->part;
+        LimbPtrs lp{};
+        for (uint32_t r = 0; r < G; ++r)
+            lp.p[r] = reinterpret_cast<const unsigned long long*>(w.share[share].as<double>() + (size_t)r * P.stride +
+                                                                   P.slice);
+        k_sum_limbs<<<1, 32, 0, g->stream>>>(lp, G, limbs_total(w));
+        CKL("k_sum_limbs");
+        ++g->launches;
+    };
     if (Pg.size() == 1) {
         tpa_graph* g = Pg[0];
         Workspace& w = g->workspace(1);
         PartInfo& P = *g->part;
-        if (P.comm) {
-            NCK(nccl().AllReduce(limbs_slot(w, slot), limbs_total(w), 6, ncclUint64, ncclSum, P.comm, g->stream));
-            if (share >= 0) {
+        if (share >= 0) {
+            if (P.comm) {
                 double* buf = w.share[share].as<double>();
-                NCK(nccl().AllGather(buf + (size_t)P.rank * P.slice, buf, P.slice, ncclDouble, P.comm, g->stream));
+                NCK(nccl().AllGather(buf + (size_t)P.rank * P.stride, buf, P.stride, ncclDouble, P.comm, g->stream));
             }
+            sum_local(g);
+        } else if (P.comm) {
+            NCK(nccl().AllReduce(limbs_slot(w, slot), limbs_total(w), 6, ncclUint64, ncclSum, P.comm, g->stream));
         } else {
             CK(cudaMemcpyAsync(limbs_total(w), limbs_slot(w, slot), 48, cudaMemcpyDeviceToDevice, g->stream));
         }
@@ -259,17 +286,19 @@ static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share) {
         DeviceGuard dg(g->device);
         for (uint32_t r = 0; r < G; ++r) CK(cudaStreamWaitEvent(g->stream, ev[r], 0));
         Workspace& w = g->workspace(1);
-        k_sum_limbs<<<1, 32, 0, g->stream>>>(lp, G, limbs_total(w));
-        CKL("k_sum_limbs");
-        ++g->launches;
         if (share >= 0) {
             const PartInfo& P = *g->part;
             for (uint32_t r = 0; r < G; ++r) {
-                if (r == q || P.rows(r) == 0) continue;
-                double* dst = w.share[share].as<double>() + (size_t)r * P.slice;
-                const double* src = Pg[r]->workspace(1).share[share].as<double>() + (size_t)r * P.slice;
-                CK(cudaMemcpyPeerAsync(dst, g->device, src, Pg[r]->device, (size_t)P.rows(r) * 8, g->stream));
+                if (r == q) continue;
+                double* dst = w.share[share].as<double>() + (size_t)r * P.stride;
+                const double* src = Pg[r]->workspace(1).share[share].as<double>() + (size_t)r * P.stride;
+                CK(cudaMemcpyPeerAsync(dst, g->device, src, Pg[r]->device, (size_t)P.stride * 8, g->stream));
             }
+            sum_local(g);
+        } else {
+            k_sum_limbs<<<1, 32, 0, g->stream>>>(lp, G, limbs_total(w));
+            CKL("k_sum_limbs");
+            ++g->launches;
         }
     }
     // the events are reusable once the waits are enqueued
@@ -310,12 +339,12 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
             const int nblk = grid_for(nl, 4 * kThreads, 4 * g->num_sms);
             k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.seeds ? dx[k].as<double>() : nullptr, weight, nl,
                                                            g->deg.as<uint32_t>(), keep,
-                                                           w.share[0].as<double>() + (size_t)P.rank * P.slice,
+                                                           w.share[0].as<double>() + (size_t)P.rank * P.stride,
                                                            acc0, w.fx.as<unsigned long long>());
             CKL("k_init_dense");
         }
-        k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), limbs_slot(w, 2), g->policy, keep, n,
-                                              active0, w.state.as<ColState>());
+        k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), limbs_at(g, 2, 0), g->policy, keep,
+                                              n, active0, w.state.as<ColState>());
         CKL("k_init_finish");
         g->launches += 2;
         StepArgs& a = A[k];
@@ -368,12 +397,12 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
                 ColState* st = w.state.as<ColState>();
                 a.step = i;
                 a.share_in = w.share[(i - 1) & 1].as<double>();
-                a.share_out = last ? nullptr : w.share[i & 1].as<double>() + (size_t)P.rank * P.slice;
+                a.share_out = last ? nullptr : w.share[i & 1].as<double>() + (size_t)P.rank * P.stride;
                 a.acc = inw ? w.acc.as<double>() : nullptr;
                 a.state_in = st + ((i - 1) & 1);
                 a.state_out = st + (i & 1);
                 if (g->n) launch_step(g, w, a, nullptr, 1);
-                else CK(cudaMemsetAsync(limbs_slot(w, i & 1), 0, 48, g->stream));  // empty partition
+                else CK(cudaMemsetAsync(limbs_at(g, (int)(i & 1), last ? -1 : (int)(i & 1)), 0, 48, g->stream));
             }
             part_exchange(Pg, (int)(i & 1), last ? -1 : (int)(i & 1));
             for (size_t k = 0; k < Pg.size(); ++k) {
