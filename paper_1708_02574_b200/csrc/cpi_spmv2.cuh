@@ -20,11 +20,22 @@
 
 namespace tpa {
 
+// In-process partition groups (tpa_part.cuh): the sweep stores each share
+// (and its limbs) into every other partition's buffer too -- peer stores over
+// NVLink that overlap the sweep instead of a copy step after it.
+constexpr int kMaxPeerOut = 15;
+struct PeerOut {
+    double* p[kMaxPeerOut];  // the same span of each peer's share_out buffer
+    uint32_t n;
+};
+
 struct MvArgs {
     StepArgs s;
     const longlong2* __restrict__ item_nnz;  // [n_items] {nnz begin, nnz end}
     unsigned long long* fx;                  // [4]: l1 hi/lo, dm hi/lo; zero between launches
     unsigned long long* limbs;               // partition mode: [6] out (see fx_to_limbs), else null
+    PeerOut peers;                           // partition group: replicas of share_out (n = 0: none)
+    uint32_t limb_off;                       // limbs - share_out, in doubles (peer copies of the limbs)
 };
 
 // 128-bit fixed-point totals as three limbs each (hi, lo >> 32, lo & 2^32-1):
@@ -167,7 +178,11 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
                     a.acc[vtx] = f;
                 }
             }
-            if (a.share_out) a.share_out[vtx] = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
+            if (a.share_out) {
+                const double sv = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
+                a.share_out[vtx] = sv;
+                for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][vtx] = sv;
+            }
             my_l1 = dadd(my_l1, fabs(y));
             if (want_dm && dg[q] == 0) my_dm = dadd(my_dm, y);
         }
@@ -191,6 +206,8 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
             const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
+            if (a.share_out)
+                for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][rb] = d ? ddiv(dmul(a.keep, y), (double)d) : 0.0;
             my_l1 = fabs(y);
             if (want_dm && d == 0) my_dm = y;
         }
@@ -221,6 +238,11 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         // a partition's totals: all-reduced, then k_part_finalize advances the state
         fx_to_limbs(h0, l0, M.limbs);
         fx_to_limbs(h1, l1, M.limbs + 3);
+        for (uint32_t k = 0; k < M.peers.n; ++k) {
+            auto* pl = reinterpret_cast<unsigned long long*>(M.peers.p[k] + M.limb_off);
+            fx_to_limbs(h0, l0, pl);
+            fx_to_limbs(h1, l1, pl + 3);
+        }
     } else {
         // last CTA: cpi.cpp:73-80
         a.state_out[0] = advance_state(st, fx_decode(h0, l0), fx_decode(h1, l1), a);

@@ -510,6 +510,7 @@ struct tpa_graph {
     } pipe;
     std::set<tpa_artifact*> artifacts;  // detached (buffers freed) on destroy
     std::unique_ptr<PartInfo> part;     // row partition (multi-GPU), or null: whole graph
+    PeerOut peer_out{};                 // set by the group driver around a sweep (tpa_part.cuh)
     struct TopkWork {
         DevBuf st, hist, cand, ids;  // device top-k (tpa_topk.cuh): state, histograms, candidates, picks
     } topk;
@@ -814,11 +815,13 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                     return e != nullptr;
                 }();
                 (void)carve;
-                k_step_spmv2<<<grid, block, 0, g->stream>>>(MvArgs{
-                    a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
-                    !g->part ? nullptr
-                    : a.share_out ? reinterpret_cast<unsigned long long*>(a.share_out + g->part->slice)
-                                  : w.limbs.as<unsigned long long>() + (a.step & 1) * 6});
+                MvArgs M{a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
+                         !g->part ? nullptr
+                         : a.share_out ? reinterpret_cast<unsigned long long*>(a.share_out + g->part->slice)
+                                       : w.limbs.as<unsigned long long>() + (a.step & 1) * 6,
+                         PeerOut{}, g->part ? g->part->slice : 0u};
+                if (g->part && a.share_out) M.peers = g->peer_out;
+                k_step_spmv2<<<grid, block, 0, g->stream>>>(M);
             }
             else
                 k_step_spmv<<<grid, block, 0, g->stream>>>(a);

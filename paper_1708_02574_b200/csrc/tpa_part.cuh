@@ -242,7 +242,7 @@ static unsigned long long* limbs_at(tpa_graph* g, int slot, int share) {
 // Every partition's totals for `slot`: with a share buffer, one in-place
 // all-gather of the spans (shares + limbs) and a local sum of the G limb
 // sets; without, an all-reduce of the limbs.  Stream-ordered, no host sync.
-static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share) {
+static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share, bool stored = false) {
     const uint32_t G = Pg[0]->part->nranks;
     auto sum_local = [&](tpa_graph* g) {  // the G limb sets of g's gathered buffer
         Workspace& w = g->workspace(1);
@@ -288,7 +288,7 @@ static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share) {
         Workspace& w = g->workspace(1);
         if (share >= 0) {
             const PartInfo& P = *g->part;
-            for (uint32_t r = 0; r < G; ++r) {
+            for (uint32_t r = 0; r < G && !stored; ++r) {  // stored: the sweep already wrote the peers
                 if (r == q) continue;
                 double* dst = w.share[share].as<double>() + (size_t)r * P.stride;
                 const double* src = Pg[r]->workspace(1).share[share].as<double>() + (size_t)r * P.stride;
@@ -388,12 +388,21 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
             const uint32_t i = (uint32_t)(done + 1 + j);
             const bool last = (int64_t)i == target;
             const bool inw = i >= cfg.start && (cfg.terminal < 0 || (int64_t)i <= cfg.terminal);
+            // in-process groups: each sweep stores its shares into the peers' buffers
+            const bool fused = Pg.size() > 1 && Pg.size() <= (size_t)kMaxPeerOut + 1 && !last &&
+                               !std::getenv("TPA_GROUP_COPY");
             for (size_t k = 0; k < Pg.size(); ++k) {
                 tpa_graph* g = Pg[k];
                 DeviceGuard dg(g->device);
                 Workspace& w = g->workspace(1);
                 const PartInfo& P = *g->part;
                 StepArgs& a = A[k];
+                g->peer_out = PeerOut{};
+                if (fused)
+                    for (size_t q = 0; q < Pg.size(); ++q)
+                        if (q != k)
+                            g->peer_out.p[g->peer_out.n++] =
+                                Pg[q]->workspace(1).share[i & 1].as<double>() + (size_t)P.rank * P.stride;
                 ColState* st = w.state.as<ColState>();
                 a.step = i;
                 a.share_in = w.share[(i - 1) & 1].as<double>();
@@ -401,10 +410,16 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
                 a.acc = inw ? w.acc.as<double>() : nullptr;
                 a.state_in = st + ((i - 1) & 1);
                 a.state_out = st + (i & 1);
-                if (g->n) launch_step(g, w, a, nullptr, 1);
-                else CK(cudaMemsetAsync(limbs_at(g, (int)(i & 1), last ? -1 : (int)(i & 1)), 0, 48, g->stream));
+                if (g->n) {
+                    launch_step(g, w, a, nullptr, 1);
+                } else {  // an empty partition publishes zero totals (to the peers too)
+                    CK(cudaMemsetAsync(limbs_at(g, (int)(i & 1), last ? -1 : (int)(i & 1)), 0, 48, g->stream));
+                    for (uint32_t q = 0; q < g->peer_out.n; ++q)
+                        CK(cudaMemsetAsync(g->peer_out.p[q] + P.slice, 0, 48, g->stream));
+                }
+                g->peer_out = PeerOut{};
             }
-            part_exchange(Pg, (int)(i & 1), last ? -1 : (int)(i & 1));
+            part_exchange(Pg, (int)(i & 1), last ? -1 : (int)(i & 1), fused);
             for (size_t k = 0; k < Pg.size(); ++k) {
                 tpa_graph* g = Pg[k];
                 DeviceGuard dg(g->device);
