@@ -362,3 +362,31 @@ def test_c1_config_full(oracle):
     qs = P.query_batch(g, art, seeds[1:], 5)
     for k in range(0, 64, 9):
         assert_close(qs[k], oracle.query(g, want, 0.15, 1e-9, 10, int(seeds[1 + k]), 5))
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_c2_config_full(oracle):
+    """BASELINE configs[1] at full size: R-MAT 20, ef 16 (16.6 M edges).  The
+    stranger vector and sampled queries against the oracle; all 1,024 queries of
+    the bench job through the closed-form mass identity (SelfLoop conserves mass:
+    ||family||_1 = 1 - (1-c)^S, ||stranger||_1 = (1-c)^T within eps/c)."""
+    import torch
+    c, eps, S, T = 0.15, 1e-9, 5, 10
+    g = P.generate_rmat(20, 16, rng_seed=1)
+    art = P.preprocess(g, c, eps, T)
+    want = oracle.preprocess(g, c, eps, T)
+    assert_close(art.stranger_scores, want, what="C2 stranger")
+    seeds = P.sample_seeds(g, 1024, 1)
+    out = torch.empty((32, g.node_count()), dtype=torch.float64, device="cuda")
+    nsf = P.neighbor_scale_factor(c, S, T)
+    mass = (1 + nsf) * (1 - (1 - c) ** S) + (1 - c) ** T
+    for b0 in range(0, 1024, 32):
+        P.query_batch(g, art, seeds[b0:b0 + 32], S, out=out)
+        sums = out.sum(dim=1).cpu().numpy()
+        assert np.all(np.abs(sums - mass) <= eps / c), (b0, sums.min(), sums.max())
+        if b0 % 256 == 0:
+            host = out.cpu().numpy()
+            for k in (0, 31):
+                assert_close(host[k], oracle.query(g, want, c, eps, T, int(seeds[b0 + k]), S),
+                             what=f"C2 query {b0 + k}")
