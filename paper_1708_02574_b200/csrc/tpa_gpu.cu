@@ -357,7 +357,11 @@ static int mm5_rows(int B, uint32_t step) {
         return (v == 4 || v == 8 || v == 16) ? v : 0;
     }();
     if (env) return env;
-    if (B == 32) return step <= 1 ? 16 : 8;
+    static const uint32_t wide_steps = [] {  // A/B: sweeps 1..k in 16-row blocks
+        const char* e = std::getenv("TPA_MM5_WIDE_STEPS");
+        return e ? (uint32_t)std::atoi(e) : 0u;
+    }();
+    if (B == 32) return step <= wide_steps ? 16 : 8;
     return 8;
 }
 
@@ -742,7 +746,8 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             if (by_win) CK(cudaMemsetAsync(w.wbits.p, 0, ((size_t)(g->n >> rb_shift) / 32 + 1) * 4, g->stream));
             uint32_t* wl_cnt = reinterpret_cast<uint32_t*>(w.sparse_ctl.as<char>() + 12);
             const int gb = grid_for(words, 8, 16 * g->num_sms);
-            k_frontier_cost<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(), ctl);
+            k_frontier_cost<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(), ctl,
+                                                       a.state_in, B);
             CKL("k_frontier_cost");
             MarkArgs MA{mm->nz_in, words, g->out_off.as<uint64_t>(), g->out_tgt.as<uint32_t>(), ctl,
                         g->m / g->sparse_div, w.rowflag.as<uint8_t>(), reinterpret_cast<int*>(ctl + 1),

@@ -390,3 +390,22 @@ def test_c2_config_full(oracle):
             for k in (0, 31):
                 assert_close(host[k], oracle.query(g, want, c, eps, T, int(seeds[b0 + k]), S),
                              what=f"C2 query {b0 + k}")
+
+
+@pytest.mark.gpu
+def test_uniform_spread_disables_sparse_pull(oracle):
+    """A small frontier that reaches dangling nodes (Uniform policy): the next
+    sweep carries a spread onto every row, so it must not take the sparse
+    (frontier-reachable rows only) pull."""
+    rng = np.random.default_rng(11)
+    n, live, k = 200_000, 150_000, 8
+    src = np.repeat(np.arange(live, dtype=np.uint32), k)
+    dst = rng.integers(0, n, src.size, dtype=np.uint32)  # ~25% of targets are dangling sinks
+    g = P.Graph(n, (src, dst), "uniform")
+    art = P.preprocess(g, 0.15, 1e-9, 10)
+    want = oracle.preprocess(g, 0.15, 1e-9, 10)
+    assert_close(art.stranger_scores, want, what="stranger")
+    seeds = np.arange(0, 32 * 997, 997, dtype=np.uint32)
+    out = P.query_batch(g, art, seeds, 5)
+    for j in (0, 13, 31):
+        assert_close(out[j], oracle.query(g, want, 0.15, 1e-9, 10, int(seeds[j]), 5), what=f"seed {seeds[j]}")
