@@ -55,15 +55,12 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     const StepArgs& a = A.s;
     extern __shared__ __align__(16) unsigned char s_dyn[];
     __shared__ ColState s_st[B];
-    __shared__ uint32_t s_q[Sh::NW][2][16];  // sparse scan: queued live (source, row) per warp
     __shared__ unsigned long long s_fx[4 * B];
     __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int c0 = lane * CPL;
     double (*yb)[B] = reinterpret_cast<double (*)[B]>(s_dyn + (size_t)wid * Sh::kWarpBytes);
-    uint32_t* sq_u = s_q[wid][0];
-    uint32_t* sq_k = s_q[wid][1];
     double* tile = reinterpret_cast<double*>(s_dyn + (size_t)wid * Sh::kWarpBytes + Sh::kYBytes);
 
     for (int i = tid; i < 4 * B; i += Sh::NT) s_fx[i] = 0ull;
@@ -182,54 +179,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         auto bits_at = [&](uint32_t u, int64_t base) -> uint32_t {
             return (nz && lane < U && base + lane < e1) ? __ldg(nz + (u >> 5)) : 0xffffffffu;
         };
-        const bool sparse_scan = use_mask && !kLast;
-        if (any_active && e1 > e0 && sparse_scan) {
-            // sparse sweep: few sources are live.  Scan 32 nnz per step (lane =
-            // nnz, frontier bit), queue the live ones in order, and gather them
-            // 16 at a time (lane = column) into the row sums in shared memory --
-            // ascending sources within a row, as the dense loop.
-            __syncwarp();
-            int qn = 0;
-            auto flush = [&]() {
-                __syncwarp();
-                // unused slots gather the all-zero row and add +0.0 (no change)
-                double v[U][CPL];
-#pragma unroll
-                for (int j = 0; j < U; ++j)
-                    ld_cols<CPL>(share + (size_t)(j < qn ? sq_u[j] : A.zero_row) * B + c0, v[j]);
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int k = j < qn ? (int)sq_k[j] : 0;
-#pragma unroll
-                    for (int c = 0; c < CPL; ++c) yb[k][c0 + c] = dadd(yb[k][c0 + c], v[j][c]);
-                }
-                qn = 0;
-                __syncwarp();
-            };
-            const bool ne_row = lane < nrows && rpn > rpl;
-            for (int64_t base = e0; base < e1; base += 32) {
-                const int64_t e = base + lane;
-                const uint32_t u = e < e1 ? ld_stream_u32(col + e) : 0u;
-                const bool live = e < e1 && (!nz || ((__ldg(nz + (u >> 5)) >> (u & 31)) & 1u));
-                uint32_t lm = __ballot_sync(0xffffffffu, live);
-                while (lm) {
-                    const int j = __ffs(lm) - 1;
-                    lm &= lm - 1;
-                    const uint32_t uj = __shfl_sync(0xffffffffu, u, j);
-                    int k = 0;
-                    if (!is_seg) {  // the nonempty row holding position base + j
-                        const uint32_t km = __ballot_sync(0xffffffffu, ne_row && rpl <= base + j);
-                        k = 31 - __clz(km);
-                    }
-                    if (lane == 0) {
-                        sq_u[qn] = uj;
-                        sq_k[qn] = k;
-                    }
-                    if (++qn == U) flush();
-                }
-            }
-            if (qn) flush();
-        } else if (any_active && e1 > e0) {
+        if (any_active && e1 > e0) {
             uint32_t i0 = idx_at(e0), i1 = idx_at(e0 + U);
             uint32_t w0 = bits_at(i0, e0);
             for (int64_t base = e0; base < e1; base += U) {
@@ -293,11 +243,6 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 w0 = w1;
             }
         }
-        if (sparse_scan) {
-            __syncwarp();
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) s[c] = yb[0][c0 + c];  // a segment's sum (blocks: already in yb)
-        }
         if (is_seg) {
             // publish the segment; the last one of the row combines in order
 #pragma unroll
@@ -319,7 +264,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             if (lane == 0) A.long_cnt[li] = 0;
             if (a.acc && ((av >> (r0 & 31)) & 1u)) cp_async_acc<CPL>(tile + c0, a.acc + (size_t)r0 * B + c0);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
-        } else if (ne_mask && !sparse_scan) {
+        } else if (ne_mask) {
 #pragma unroll
             for (int c = 0; c < CPL; ++c) yb[cur][c0 + c] = s[c];
         }
