@@ -60,7 +60,7 @@ struct Mm4Args {
 __global__ void __launch_bounds__(256) k_frontier_cost(const uint32_t* __restrict__ nz, uint32_t n_words,
                                                        const uint64_t* __restrict__ out_off,
                                                        unsigned long long* cost, const ColState* __restrict__ st,
-                                                       int B) {
+                                                       int B, unsigned long long limit) {
     const int lane = threadIdx.x & 31;
     // a Uniform spread reaches every row (graph.cpp:265-268): no sparse pull then
 #ifndef TPA_NO_SPREAD_GUARD  // (A/B only: reproduces the unguarded decision)
@@ -69,11 +69,23 @@ __global__ void __launch_bounds__(256) k_frontier_cost(const uint32_t* __restric
 #endif
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     unsigned long long c = 0;
-    for (uint32_t w = gw; w < n_words; w += nw) {
+    uint32_t k = 0;
+    for (uint32_t w = gw; w < n_words; w += nw, ++k) {
+        // a dense frontier: stop once the running total is past the limit
+        if ((k & 7) == 7) {
+            const int over = lane == 0 && *reinterpret_cast<volatile unsigned long long*>(cost) > limit;
+            if (__shfl_sync(0xffffffffu, over, 0)) break;  // warp-uniform
+        }
         const uint32_t bits = __ldg(nz + w);
         if ((bits >> lane) & 1u) {
             const uint32_t u = w * 32 + lane;
             c += __ldg(out_off + u + 1) - __ldg(out_off + u);
+        }
+        if ((k & 7) == 7) {  // publish the partial total every 8 words
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0 && c) atomicAdd(cost, c);
+            c = 0;
         }
     }
 #pragma unroll

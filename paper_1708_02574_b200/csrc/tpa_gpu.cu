@@ -747,7 +747,7 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             uint32_t* wl_cnt = reinterpret_cast<uint32_t*>(w.sparse_ctl.as<char>() + 12);
             const int gb = grid_for(words, 8, 16 * g->num_sms);
             k_frontier_cost<<<gb, 256, 0, g->stream>>>(mm->nz_in, words, g->out_off.as<uint64_t>(), ctl,
-                                                       a.state_in, B);
+                                                       a.state_in, B, g->m / g->sparse_div);
             CKL("k_frontier_cost");
             MarkArgs MA{mm->nz_in, words, g->out_off.as<uint64_t>(), g->out_tgt.as<uint32_t>(), ctl,
                         g->m / g->sparse_div, w.rowflag.as<uint8_t>(), reinterpret_cast<int*>(ctl + 1),
