@@ -249,7 +249,8 @@ def run_reference_arm(args):
     cb = dict(cb, value=v)
     line = {"impl": "reference", "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",
             "value": v, "unit": "GTEPS", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": cb["job_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": cb["job_s"] * 1e3, "higher_is_better": True,
+            "scaling": "strong" if args.gpus > 1 else "weak",  # one job, as our arm's N > 1 line
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_desc(cfg_name, g, nq, batch), "queries_per_s": cb["queries_per_s"],
             "cpu_baseline": cb,
@@ -422,6 +423,14 @@ def run_ours(args):
         avg_ms = mv_ms / max(mv_cnt, 1)
         share = mv_ms / total_ms if total_ms else None
     achieved = bytes_launch / (avg_ms / 1e3) / 1e9
+    # the access pattern's own ceiling (profiles/microbench.json): the sweeps are
+    # gather-bound (L2 -> SM for the SpMM rows, L1 request rate for the SpMV)
+    mb = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "microbench.json")) as f:
+            mb = json.load(f)
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": traffic_per_launch(kname), "algorithmic_bytes_per_launch": bytes_launch,
@@ -431,6 +440,16 @@ def run_ours(args):
                 "spmv": {"launches": mv_cnt, "avg_ms": mv_ms / max(mv_cnt, 1),
                          "achieved_gbs": a_step(n, m, 1, 1) / (mv_ms / max(mv_cnt, 1) / 1e3) / 1e9
                          if mv_cnt else None}}
+    if batch > 1 and mb.get("gather_256B_rows"):
+        g_gbs = m * Bk * 8 / (avg_ms / 1e3) / 1e9  # every nonzero gathers one B-wide share row
+        pk = mb["gather_256B_rows"]["best_gbs"] if Bk == 32 else None
+        roofline["gather_bound"] = {"achieved_gbs": g_gbs, "peak_gbs": pk, "frac": g_gbs / pk if pk else None,
+                                    "source": "profiles/microbench.json (tools/gather_micro.cu)"}
+    if mv_cnt and mb.get("gather_8B"):
+        rate = m / (mv_ms / mv_cnt / 1e3)
+        roofline["spmv"]["gather_bound"] = {"achieved_gathers_per_s": rate,
+                                            "peak_gathers_per_s": mb["gather_8B"]["best_gathers_per_s"],
+                                            "frac": rate / mb["gather_8B"]["best_gathers_per_s"]}
 
     # end-to-end through the public API with host buffers
     e2e = None
