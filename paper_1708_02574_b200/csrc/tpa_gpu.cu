@@ -608,8 +608,10 @@ struct tpa_graph {
             }
             w.grid = std::max(1, occ) * num_sms;
             if (spmm_version(B) >= 4) {
-                w.Y.ensure((size_t)n * B * 8, stream);
-                w.ybits.ensure(words * 4, stream);
+                if (spmm_version(B) == 4) {  // v4's row sums round-trip HBM (n x B doubles)
+                    w.Y.ensure((size_t)n * B * 8, stream);
+                    w.ybits.ensure(words * 4, stream);
+                }
                 w.rowflag.ensure((size_t)n + 16, stream);
                 w.sparse_ctl.ensure(32, stream);
                 w.big.ensure(mark_chunk_cap(m) * sizeof(ulonglong2), stream);
