@@ -172,70 +172,78 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             }
             cur = k_next;
         };
-        auto idx_at = [&](int64_t base) -> uint32_t {
+        // indices 32 at a time (every lane), two windows ahead of use; the
+        // U-wide gather groups take their sources from the window by shuffle
+        auto idx32 = [&](int64_t base) -> uint32_t {
             const int64_t e = base + lane;
-            return (lane < U && e < e1) ? ld_stream_u32(col + e) : 0u;
+            return e < e1 ? ld_stream_u32(col + e) : 0u;
         };
-        auto bits_at = [&](uint32_t u, int64_t base) -> uint32_t {
-            return (nz && lane < U && base + lane < e1) ? __ldg(nz + (u >> 5)) : 0xffffffffu;
+        auto bits32 = [&](uint32_t u, int64_t base) -> uint32_t {
+            return (nz && base + lane < e1) ? __ldg(nz + (u >> 5)) : 0xffffffffu;
         };
         if (any_active && e1 > e0) {
-            uint32_t i0 = idx_at(e0), i1 = idx_at(e0 + U);
-            uint32_t w0 = bits_at(i0, e0);
-            for (int64_t base = e0; base < e1; base += U) {
-                const uint32_t i2 = idx_at(base + 2 * U);
-                const uint32_t w1 = bits_at(i1, base + U);
-                const bool live = (w0 >> (i0 & 31)) & 1u;
-                const uint32_t lmask = __ballot_sync(0xffffffffu, live && lane < U && base + lane < e1);
-                const int64_t p = rpl - base;
-                const uint32_t smask = __ballot_sync(0xffffffffu, starts && p >= 0 && p < U);
-                if (lmask) {
-                    double v[U][CPL];
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const uint32_t u = __shfl_sync(0xffffffffu, i0, j);
-                        if ((lmask >> j) & 1u) {
-                            ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
-                        }
-                    }
-                    if (smask == 0) {
-#pragma unroll
-                        for (int j = 0; j < U; ++j)
-#pragma unroll
-                            for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
-                    } else {
-                        uint32_t m = smask;
-                        int pos_next = U, k_next = 0;
-                        if (m) {
-                            k_next = __ffs(m) - 1;
-                            m &= m - 1;
-                            pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
-                        }
+            uint32_t i0 = idx32(e0), i1 = idx32(e0 + 32);
+            uint32_t w0 = bits32(i0, e0);
+            for (int64_t wbase = e0; wbase < e1; wbase += 32) {
+                const uint32_t i2 = idx32(wbase + 64);
+                const uint32_t w1 = bits32(i1, wbase + 32);
+                const uint32_t live32 =
+                    __ballot_sync(0xffffffffu, ((w0 >> (i0 & 31)) & 1u) && wbase + lane < e1);
+#pragma unroll 1
+                for (int h = 0; h < 32 / U; ++h) {
+                    const int64_t base = wbase + h * U;
+                    if (base >= e1) break;  // warp-uniform
+                    const uint32_t lmask = (live32 >> (h * U)) & ((1u << U) - 1u);
+                    const int64_t p = rpl - base;
+                    const uint32_t smask = __ballot_sync(0xffffffffu, starts && p >= 0 && p < U);
+                    if (lmask) {
+                        double v[U][CPL];
 #pragma unroll
                         for (int j = 0; j < U; ++j) {
-                            if (j == pos_next) {  // warp-uniform
-                                close_row(k_next);
-                                if (m) {
-                                    k_next = __ffs(m) - 1;
-                                    m &= m - 1;
-                                    pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
-                                } else {
-                                    pos_next = U;
-                                }
+                            const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
+                            if ((lmask >> j) & 1u) {
+                                ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
+                            }
+                        }
+                        if (smask == 0) {
+#pragma unroll
+                            for (int j = 0; j < U; ++j)
+#pragma unroll
+                                for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                        } else {
+                            uint32_t m = smask;
+                            int pos_next = U, k_next = 0;
+                            if (m) {
+                                k_next = __ffs(m) - 1;
+                                m &= m - 1;
+                                pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
                             }
 #pragma unroll
-                            for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                            for (int j = 0; j < U; ++j) {
+                                if (j == pos_next) {  // warp-uniform
+                                    close_row(k_next);
+                                    if (m) {
+                                        k_next = __ffs(m) - 1;
+                                        m &= m - 1;
+                                        pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
+                                    } else {
+                                        pos_next = U;
+                                    }
+                                }
+#pragma unroll
+                                for (int c = 0; c < CPL; ++c) s[c] = dadd(s[c], v[j][c]);
+                            }
                         }
-                    }
-                } else if (smask) {
-                    uint32_t m = smask;
-                    while (m) {
-                        const int k = __ffs(m) - 1;
-                        m &= m - 1;
-                        close_row(k);
+                    } else if (smask) {
+                        uint32_t m = smask;
+                        while (m) {
+                            const int k = __ffs(m) - 1;
+                            m &= m - 1;
+                            close_row(k);
+                        }
                     }
                 }
                 i0 = i1;
