@@ -371,6 +371,9 @@ static void launch_fused(const Mm4Args& P, int num_sms, cudaStream_t stream) {
     static const int grid = [num_sms] {
         CK(cudaFuncSetAttribute(k_mm_fused<B, L, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)Sh::kDynSmem));
+        if (const char* e = std::getenv("TPA_MM5_CARVEOUT"))  // A/B: shared memory vs L1 split
+            CK(cudaFuncSetAttribute(k_mm_fused<B, L, RB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    std::atoi(e)));
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mm_fused<B, L, RB>, Sh::NT, Sh::kDynSmem));
         return std::max(occ, 1) * num_sms;
