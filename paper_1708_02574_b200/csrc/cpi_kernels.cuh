@@ -238,9 +238,10 @@ __device__ __forceinline__ void combine_only(const StepArgs& a, uint32_t v, uint
 // staged through shared memory, or one long row reduced by the whole CTA.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_step_spmv(StepArgs a) {
-    __shared__ double s_vals[kMvTileNnz];
-    __shared__ int64_t s_rp[kMvTileRows + 1];
-    __shared__ double s_y[kMvTileRows];
+    extern __shared__ __align__(16) unsigned char s_mv1[];  // kMvTileNnz + 2 kMvTileRows + 1 words
+    double* s_vals = reinterpret_cast<double*>(s_mv1);
+    int64_t* s_rp = reinterpret_cast<int64_t*>(s_vals + kMvTileNnz);
+    double* s_y = reinterpret_cast<double*>(s_rp + kMvTileRows + 1);
     __shared__ double s_red[kThreads];
     __shared__ double s_fin[kThreads];
     __shared__ double s_part[2];

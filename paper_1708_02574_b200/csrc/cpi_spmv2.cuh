@@ -29,6 +29,8 @@ struct PeerOut {
     uint32_t n;
 };
 
+constexpr size_t kMvDynSmem = (size_t)kMvTileNnz * 8 + (kMvTileRows + 1) * 8 + (size_t)kMvTileRows * 8;
+
 struct MvArgs {
     StepArgs s;
     const longlong2* __restrict__ item_nnz;  // [n_items] {nnz begin, nnz end}
@@ -72,9 +74,12 @@ __global__ void __launch_bounds__(kThreads, TPA_MV2_MINB) k_step_spmv2(MvArgs M)
 __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
 #endif
     const StepArgs& a = M.s;
-    __shared__ double s_vals[kMvTileNnz];
-    __shared__ int64_t s_rp[kMvTileRows + 1];
-    __shared__ double s_y[kMvTileRows];
+    // the tile's staging in dynamic shared memory (kMvDynSmem bytes): values,
+    // row pointers, row sums
+    extern __shared__ __align__(16) unsigned char s_mv[];
+    double* s_vals = reinterpret_cast<double*>(s_mv);
+    int64_t* s_rp = reinterpret_cast<int64_t*>(s_vals + kMvTileNnz);
+    double* s_y = reinterpret_cast<double*>(s_rp + kMvTileRows + 1);
     __shared__ double s_red[kThreads];
     __shared__ uint32_t s_ticket;
 

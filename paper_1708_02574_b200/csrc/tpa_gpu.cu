@@ -831,10 +831,24 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                                        : w.limbs.as<unsigned long long>() + (a.step & 1) * 6,
                          PeerOut{}, g->part ? g->part->slice : 0u};
                 if (g->part && a.share_out) M.peers = g->peer_out;
-                k_step_spmv2<<<grid, block, 0, g->stream>>>(M);
+                static const bool smem_ok = [] {
+                    CK(cudaFuncSetAttribute(k_step_spmv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kMvDynSmem));
+                    return true;
+                }();
+                (void)smem_ok;
+                k_step_spmv2<<<grid, block, kMvDynSmem, g->stream>>>(M);
             }
             else
-                k_step_spmv<<<grid, block, 0, g->stream>>>(a);
+            {
+                static const bool smem1 = [] {
+                    CK(cudaFuncSetAttribute(k_step_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kMvDynSmem));
+                    return true;
+                }();
+                (void)smem1;
+                k_step_spmv<<<grid, block, kMvDynSmem, g->stream>>>(a);
+            }
             break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
         case 16: k_step_spmm2<16><<<grid, MmShape<16>::NT, MmShape<16>::kDynSmem, g->stream>>>(*mm); break;
