@@ -61,6 +61,12 @@ struct ColState {
     int32_t has_spread; // dm != 0 under Uniform
 };
 
+// Up to 64 seeds travel as a kernel parameter: no host->device copy, so
+// back-to-back query batches never wait on a staging buffer.
+struct SeedList {
+    uint32_t s[64];
+};
+
 struct StepArgs {
     const int64_t* __restrict__ row_ptr;  // CSR(Ãᵀ) n+1
     const uint32_t* __restrict__ col;     // m, ascending per row

@@ -149,8 +149,15 @@ __device__ __forceinline__ void fx_cta_flush(unsigned long long f0, unsigned lon
             h1 += s_w[4 * k + 2] + (t < l1 ? 1ull : 0ull);
             l1 = t;
         }
-        if (h0 | l0) fx_atomic_add(&fx[0], &fx[1], h0, l0);
-        if (h1 | l1) fx_atomic_add(&fx[2], &fx[3], h1, l1);
+        if (fx) {
+            if (h0 | l0) fx_atomic_add(&fx[0], &fx[1], h0, l0);
+            if (h1 | l1) fx_atomic_add(&fx[2], &fx[3], h1, l1);
+        } else {  // no target: the CTA totals stay in s_w[0..3] (thread 0)
+            s_w[0] = h0;
+            s_w[1] = l0;
+            s_w[2] = h1;
+            s_w[3] = l1;
+        }
     }
 }
 

@@ -32,6 +32,7 @@
 #include "cpi_spmm4.cuh"
 #include "cpi_spmm5.cuh"
 #include "cpi_spmv3.cuh"
+#include "cpi_sweep1.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
 
@@ -184,11 +185,6 @@ __global__ void k_init_finish(unsigned long long* fx, unsigned long long* limbs,
     fx[0] = fx[1] = fx[2] = fx[3] = 0ull;
 }
 
-// Up to 64 seeds travel as a kernel parameter: no host->device copy, so
-// back-to-back query batches never wait on a staging buffer.
-struct SeedList {
-    uint32_t s[64];
-};
 
 // Batch of single-seed starts x⁽⁰⁾_b = c·e_{seed_b}; share0/acc0 pre-zeroed.
 __global__ void k_init_seeds(const SeedList seeds, uint32_t b_valid, int B, double c,
@@ -441,6 +437,7 @@ struct Workspace {
     DevBuf share[2], acc, part, gpart, group_cnt, done_cnt, state;
     // SpMM (B > 1) extras
     DevBuf nz[2], acc_valid, long_cnt, seg_part, work_cnt, fx;
+    DevBuf s1_skip, s1_fx;  // the seed push took sweep 1 (cpi_sweep1.cuh); its exact totals
     int grid = 0;  // persistent grid of k_step_spmm2<B>
     DevBuf Y, ybits;  // v4: row sums and their written-rows bitmap
     DevBuf rowflag, sparse_ctl;  // sparse sweeps: reachable rows; {cost, dense, window count}
@@ -526,6 +523,7 @@ struct tpa_graph {
     std::mutex mu;
     bool sparse_off = std::getenv("TPA_NO_SPARSE") != nullptr;  // A/B switch
     bool no_window_list = std::getenv("TPA_NO_WINDOW_LIST") != nullptr;  // A/B switch
+    bool s1_push_off = std::getenv("TPA_NO_SEED_PUSH") != nullptr;       // A/B switch
     uint64_t sparse_div = [] {  // sparse sweep if the push touches <= m / sparse_div edges
         const char* e = std::getenv("TPA_SPARSE_DIV");
         const long v = e ? std::atol(e) : 32;
@@ -723,7 +721,8 @@ static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
     return std::upper_bound(bounds.begin(), bounds.end(), i) - bounds.begin();
 }
 
-static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B) {
+static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
+                        const SeedList* push_seeds = nullptr) {
     const Schedule& s = g->mv;
     const dim3 grid(B == 1 ? s.n_items : (uint32_t)w.grid), block(kThreads);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -741,7 +740,27 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         // the first sweeps of a seed batch usually see a small frontier: if it
         // pushes along at most m/32 edges, mark the rows it reaches (push over
         // the out-CSR) and pull only those; the decision is taken on the device
-        if (mm->nz_in && a.step <= kSparseSweeps && !g->sparse_off) {
+        if (push_seeds) {  // sweep 1 by a push from the seeds (cpi_sweep1.cuh): no pull
+            if (!w.s1_skip.p) {
+                w.s1_skip.ensure(16, g->stream);
+                w.s1_fx.ensure(4 * 64 * 8, g->stream);
+                CK(cudaMemsetAsync(w.s1_fx.p, 0, w.s1_fx.bytes, g->stream));
+                CK(cudaMemsetAsync(w.s1_skip.p, 0, w.s1_skip.bytes, g->stream));
+            }
+            Sweep1Args S1{a, w.s1_fx.as<unsigned long long>(), g->out_off.as<uint64_t>(),
+                          g->out_tgt.as<uint32_t>(), *push_seeds, mm->nz_out, mm->acc_valid,
+                          w.s1_skip.as<uint32_t>()};
+            const dim3 g1(8, B);  // 8 chunks per column: a hub seed's out-list is spread
+            if (B == 32) {
+                k_s1_rows<32><<<g1, 256, 0, g->stream>>>(S1);
+                k_s1_push<32><<<g1, 256, 0, g->stream>>>(S1);
+            } else {
+                k_s1_rows<64><<<g1, 256, 0, g->stream>>>(S1);
+                k_s1_push<64><<<g1, 256, 0, g->stream>>>(S1);
+            }
+            CKL("k_s1_push");
+            g->launches += 2;  // k_s1_rows + k_s1_push (the common ++ below is cancelled)
+        } else if (mm->nz_in && a.step <= kSparseSweeps && !g->sparse_off) {
             const uint32_t words = (g->n + 31) / 32;
             auto* ctl = w.sparse_ctl.as<unsigned long long>();
             CK(cudaMemsetAsync(w.sparse_ctl.p, 0, 32, g->stream));
@@ -781,7 +800,9 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                 P.sl_cnt = wl_cnt + 2;
             }
         }
-        if (spmm_version(B) == 5) {
+        if (push_seeds) {
+            g->launches -= 1;  // no pull this sweep: cancels the common ++ below
+        } else if (spmm_version(B) == 5) {
             const bool last = a.out != nullptr;
             if (B == 32) {
                 if (last) launch_fused_rb<32, true>(P, rb, g->num_sms, g->stream);
@@ -1004,7 +1025,11 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
                 ma.nz_out = a.share_out ? w.nz[i & 1].as<uint32_t>() : nullptr;
                 if (ma.nz_out) CK(cudaMemsetAsync(ma.nz_out, 0, bm_bytes, g->stream));
             }
-            launch_step(g, w, a, mm ? &ma : nullptr, B);
+            // sweep 1 of a seed batch: a push from the seeds (one term per
+            // element) instead of a pull over every nonzero
+            const bool s1 = mm && i == 1 && cfg.init == Init::Seeds && a.acc && a.share_out && !a.out &&
+                            !cfg.y_out && g->policy != kUniform && spmm_version(B) == 5 && !g->s1_push_off;
+            launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr);
         }
         done += chunk;
         if ((int64_t)done >= target) break;
