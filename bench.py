@@ -64,7 +64,16 @@ def build_graph(cfg_name):
     import paper_1708_02574_b200 as P
     kind, p, *_ = CONFIGS[cfg_name]
     if kind == "rmat":
-        return P.generate_rmat(p["scale"], p["edge_factor"], 0.57, 0.19, 0.19, rng_seed=CONFIGS[cfg_name][4])
+        # scale >= 22 (C4, C5): generated and constructed on the GPU -- the same
+        # per-chunk mt19937_64 streams, so the same graph and fingerprint as the
+        # host generator (tests/test_graph_build_gpu.py), in seconds not minutes
+        dev = None
+        if p["scale"] >= 22 and os.environ.get("TPA_HOST_GEN") != "1":
+            import torch
+            if torch.cuda.is_available():
+                dev = int(os.environ.get("LOCAL_RANK", "0"))
+        return P.generate_rmat(p["scale"], p["edge_factor"], 0.57, 0.19, 0.19, rng_seed=CONFIGS[cfg_name][4],
+                               device=dev)
     return P.generate_random_graph(p["n"], p["m"], CONFIGS[cfg_name][4])
 
 
@@ -311,7 +320,18 @@ def run_ours(args):
     h = dg.h
     import ctypes as C_
 
-    out = torch.empty((batch, n), dtype=torch.float64, device=dev)
+    # C5 (n = 2^28, B = 16): a resident [B][n] output would be 34 GB on top of
+    # the 143 GB of graph + iterate buffers, so each batch's full score
+    # vectors are written into the iterate buffer the last sweep leaves idle
+    # (tpa_query_batch_topk) and only the top-10 per seed stays resident
+    resident_topk = n * batch * 8 > (8 << 30) or os.environ.get("TPA_BENCH_TOPK") == "1"
+    K_TOP = 10
+    if resident_topk:
+        out = None
+        d_ids = torch.empty((batch, K_TOP), dtype=torch.int32, device=dev)
+        d_vals = torch.empty((batch, K_TOP), dtype=torch.float64, device=dev)
+    else:
+        out = torch.empty((batch, n), dtype=torch.float64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     batches = [np.ascontiguousarray(seeds[i:i + batch]) for i in range(0, len(seeds), batch)]
     pg = None
@@ -334,8 +354,12 @@ def run_ours(args):
             N.check(lib.tpa_artifact_create(h, d_str.data_ptr(), g.fingerprint(), C, EPS, T, N.TPA_DEVICE_PTRS,
                                             C_.byref(art)))
         for b in batches:
-            N.check(lib.tpa_query_batch(h, art, b.ctypes.data, len(b), S, out.data_ptr(),
-                                        N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
+            if resident_topk:
+                N.check(lib.tpa_query_batch_topk(h, art, b.ctypes.data, len(b), S, K_TOP, d_ids.data_ptr(),
+                                                 d_vals.data_ptr(), N.TPA_DEVICE_PTRS))
+            else:
+                N.check(lib.tpa_query_batch(h, art, b.ctypes.data, len(b), S, out.data_ptr(),
+                                            N.TPA_DEVICE_PTRS | N.TPA_ASYNC))
         return art
 
     # warm-up
@@ -453,7 +477,7 @@ def run_ours(args):
 
     # end-to-end through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not resident_topk:
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         # two pinned result buffers, alternating: batch k+1 computes while batch k drains
         host_outs = [torch.empty((batch, n), dtype=torch.float64, pin_memory=True) for _ in range(2)]
@@ -542,8 +566,13 @@ def run_ours(args):
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg_name, g, nq, batch),
             "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_topk": e2e_topk, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e if e2e is not None else e2e_topk,
+            "e2e_topk": e2e_topk, "gpu_launches": launches,
             "clocks": clk.summary(), "ingest_s": t_ingest, "graph_build_s": t_build,
+            "outputs": ("per batch: the B full score vectors written to HBM (the idle iterate buffer), then the "
+                        "device top-10 per seed kept resident (tpa_query_batch_topk)" if resident_topk else
+                        "the B full score vectors of every batch written to a resident [B][n] buffer"),
+            "device_mem_gb": torch.cuda.max_memory_reserved(dev) / 1e9 + dg.device_bytes() / 1e9,
             "parallelism": (f"row-partitioned preprocess (one NCCL all-gather per sweep: shares + exact residual limbs) + "
                             f"queries split over {world} whole-graph replicas" if partitioned else
                             f"independent replicas x{world}" if world > 1 else "single GPU"),

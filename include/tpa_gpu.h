@@ -251,6 +251,14 @@ int tpa_host_graph_rmat(uint32_t scale, uint32_t edge_factor, double a, double b
  * constructor (first out-of-range edge in input order -> TPA_ERR_OUT_OF_RANGE). */
 int tpa_host_graph_build_gpu(uint32_t n, const uint32_t *src, const uint32_t *dst, uint64_t m,
                              int policy, int device, tpa_host_graph **out);
+/* tpa_host_graph_rmat generated AND constructed on the GPU: the same
+ * per-chunk mt19937_64 streams (one thread per 2^20-edge chunk), so the
+ * edge list, the graph and its fingerprint equal the host generator's; the
+ * construction as tpa_host_graph_build_gpu (keys sorted in place: peak
+ * device memory 2 x 8 x edge_factor x 2^scale bytes).  The billion-edge
+ * configs (BASELINE C5: scale 28) are generated in seconds this way. */
+int tpa_host_graph_rmat_gpu(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                            uint64_t seed, int policy, int device, tpa_host_graph **out);
 /* generate_random_graph(n, m, seed, policy) semantics (graph.cpp:166-205). */
 int tpa_host_graph_random(uint32_t n, uint64_t m, uint64_t seed, int policy,
                           tpa_host_graph **out);

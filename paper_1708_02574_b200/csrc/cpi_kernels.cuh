@@ -377,8 +377,39 @@ template <> struct MmVec<16> { static constexpr int G = 16, CPL = 1; };
 template <> struct MmVec<32> { static constexpr int G = 32, CPL = 1; };
 template <> struct MmVec<64> { static constexpr int G = 32, CPL = 2; };
 
+// TPA_GATHER_HINT (A/B knob): 0 = plain LDG; 1 = L1::no_allocate (the row
+// gathers hit L1 ~4% of the time on dense sweeps); 2 = L1::evict_first;
+// 3 = L2::evict_last (keep the gathered share rows in L2 against the
+// streaming acc / share_out traffic).
+#ifndef TPA_GATHER_HINT
+#define TPA_GATHER_HINT 0
+#endif
 template <int CPL>
 __device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
+#if TPA_GATHER_HINT == 1
+#define TPA_GH_Q ".L1::no_allocate"
+#elif TPA_GATHER_HINT == 2
+#define TPA_GH_Q ".L1::evict_first"
+#endif
+#if TPA_GATHER_HINT == 3
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    if constexpr (CPL == 1) {
+        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(pol));
+    } else {
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+    }
+    return;
+#endif
+#ifdef TPA_GH_Q
+    if constexpr (CPL == 1) {
+        asm("ld.global.nc" TPA_GH_Q ".f64 %0, [%1];" : "=d"(v[0]) : "l"(p));
+    } else {
+        asm("ld.global.nc" TPA_GH_Q ".v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
+    }
+    return;
+#undef TPA_GH_Q
+#endif
     if constexpr (CPL == 1) {
         v[0] = __ldg(p);
     } else {

@@ -18,6 +18,11 @@
 
 namespace tpa {
 
+// TPA_EPI_STORE_HINT (A/B knob): epilogue acc / share_out stores as
+// streaming (evict-first) stores.
+#ifndef TPA_EPI_STORE_HINT
+#define TPA_EPI_STORE_HINT 0
+#endif
 #ifndef TPA_MM5_MINB
 #define TPA_MM5_MINB 8
 #endif
@@ -312,8 +317,14 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 if (kLast) {
                     tile[k * TS + c0 + c] = combine_value(a, f, r);  // tpa.cpp:73-74
                 } else {
+                    const double sh = d ? ddiv(dmul(a.keep, yy[c]), (double)d) : 0.0;  // graph.cpp:222
+#if TPA_EPI_STORE_HINT
+                    __stcs(a.acc + ix, f);
+                    __stcs(a.share_out + ix, sh);
+#else
                     a.acc[ix] = f;
-                    a.share_out[ix] = d ? ddiv(dmul(a.keep, yy[c]), (double)d) : 0.0;  // graph.cpp:222
+                    a.share_out[ix] = sh;
+#endif
                 }
                 bl1[c] = dadd(bl1[c], fabs(yy[c]));
                 if (want_dm && d == 0) bdm[c] = dadd(bdm[c], yy[c]);

@@ -104,6 +104,11 @@ struct DevBuf {
     T* as() const {
         return static_cast<T*>(p);
     }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+        std::swap(sp, o.sp);
+    }
 };
 
 // ---------------------------------------------------------------------------
@@ -1328,16 +1333,20 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         int end_bit = 1;
         while (end_bit < 32 && ((uint64_t)1 << end_bit) < n) ++end_bit;
         if (m) {
+            // double-buffered (the key / value pairs ping-pong in place): no
+            // third m-sized copy in the sort's temporary storage
+            cub::DoubleBuffer<uint32_t> kb(d_tgt.as<uint32_t>(), d_keys.as<uint32_t>());
+            cub::DoubleBuffer<uint32_t> vb(d_src.as<uint32_t>(), g->col.as<uint32_t>());
             size_t temp = 0;
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, d_tgt.as<uint32_t>(), d_keys.as<uint32_t>(),
-                                               d_src.as<uint32_t>(), g->col.as<uint32_t>(), (int64_t)m, 0,
-                                               end_bit, s));
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, kb, vb, (int64_t)m, 0, end_bit, s));
             DevBuf d_temp;
             d_temp.ensure(temp, g->stream);
-            CK(cub::DeviceRadixSort::SortPairs(d_temp.p, temp, d_tgt.as<uint32_t>(), d_keys.as<uint32_t>(),
-                                               d_src.as<uint32_t>(), g->col.as<uint32_t>(), (int64_t)m, 0,
-                                               end_bit, s));
+            CK(cub::DeviceRadixSort::SortPairs(d_temp.p, temp, kb, vb, (int64_t)m, 0, end_bit, s));
+            if (kb.Current() != d_keys.as<uint32_t>()) d_keys.swap(d_tgt);
+            if (vb.Current() != g->col.as<uint32_t>()) g->col.swap(d_src);
         }
+        d_src.release();
+        d_tgt.release();
         k_row_ptr<<<blocks, 256, 0, s>>>(d_keys.as<uint32_t>(), m, n, g->row_ptr.as<int64_t>());
         // keep the out-edge CSR (frontier push-marking of sparse sweeps)
         g->out_off.ensure((n + 1ull) * 8, g->stream);
@@ -1345,6 +1354,8 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         CK(cudaMemcpyAsync(g->out_off.p, out_offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
         if (m) CK(cudaMemcpyAsync(g->out_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
         CKL("k_row_ptr");
+        d_keys.release();
+        d_off.release();
         std::vector<int64_t> rp(n + 1ull);
         CK(cudaMemcpyAsync(rp.data(), g->row_ptr.p, (n + 1ull) * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

@@ -468,21 +468,29 @@ int tpa_query_batch_topk(tpa_graph* g, const tpa_artifact* a, const uint32_t* se
         if (B == 0) return;
         const bool dev = flags & TPA_DEVICE_PTRS;
         const double scale = 1.0 + tpa_neighbor_scale_factor(a->c, S, a->T);  // tpa.cpp:71-72
-        DevBuf buf, ids, sc;
+        DevBuf ids, sc;
         const uint32_t chunk = std::min<uint32_t>(B, 64);
-        buf.ensure((size_t)chunk * n * 8, g->stream);
         if (!dev) {
             ids.ensure((size_t)chunk * k * 4, g->stream);
             if (out_scores) sc.ensure((size_t)chunk * k * 8, g->stream);
         }
         for (uint32_t b0 = 0; b0 < B; b0 += chunk) {
             const uint32_t bv = std::min(chunk, B - b0);
+            // The combined scores land in the share buffer the batch's last
+            // sweep does not touch (sweep i reads share[(i-1)&1] and the last
+            // one, i = S-1, writes no shares; with S = 1 no sweep runs and
+            // share[1] is idle): no B x n scratch of its own, which is what
+            // lets the billion-edge config (B = 16, n = 2^28: 34 GB per
+            // buffer) fit one GPU.  Share rows are only ever read through the
+            // frontier bitmaps, so the next batch never sees these values.
+            Workspace& w = g->workspace(batch_width(bv));
+            double* scores = w.share[S == 1 ? 1 : ((S - 1) & 1)].as<double>();
             // seeds are host arrays (tpa_gpu.h); the family parts stay on the device
             run_seed_batch(g, seeds + b0, bv, a->c, a->eps, 0, (int64_t)S - 1, na ? nullptr : a->stranger.as<double>(),
-                           scale, true, buf.as<double>(), TPA_DEVICE_PTRS | TPA_ASYNC);
+                           scale, true, scores, TPA_DEVICE_PTRS | TPA_ASYNC);
             uint32_t* d_ids = dev ? out_ids + (size_t)b0 * k : ids.as<uint32_t>();
             double* d_sc = out_scores ? (dev ? out_scores + (size_t)b0 * k : sc.as<double>()) : nullptr;
-            topk_device(g, buf.as<double>(), bv, k, d_ids, d_sc);
+            topk_device(g, scores, bv, k, d_ids, d_sc);
             if (!dev) {
                 download(g, out_ids + (size_t)b0 * k, ids.p, (size_t)bv * k * 4);
                 if (out_scores) download(g, out_scores + (size_t)b0 * k, sc.p, (size_t)bv * k * 8);

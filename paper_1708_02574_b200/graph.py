@@ -175,11 +175,19 @@ def generate_random_graph(node_count: int, edge_count: int, rng_seed: int,
 
 
 def generate_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
-                  rng_seed: int = 1, policy=DanglingPolicy.SelfLoop, threads: int = 0) -> Graph:
+                  rng_seed: int = 1, policy=DanglingPolicy.SelfLoop, threads: int = 0,
+                  device: int | None = None) -> Graph:
     """R-MAT (BASELINE configs C1/C2/C4/C5): 2^scale nodes, edge_factor*2^scale raw
     edges, quadrant recursion without noise or permutation, self-loops dropped,
-    duplicates removed by the Graph construction, dangling nodes kept."""
+    duplicates removed by the Graph construction, dangling nodes kept.
+
+    ``device``: generate and construct on that GPU (same edge streams, so the
+    same graph and fingerprint; needed for the billion-edge scales)."""
     h = C.c_void_p()
+    if device is not None:
+        check(lib.tpa_host_graph_rmat_gpu(int(scale), int(edge_factor), a, b, c, int(rng_seed),
+                                          int(_policy(policy)), int(device), C.byref(h)))
+        return Graph._from_handle(h)
     check(lib.tpa_host_graph_rmat(int(scale), int(edge_factor), a, b, c, int(rng_seed), int(_policy(policy)),
                                   int(threads), C.byref(h)))
     return Graph._from_handle(h)

@@ -1,0 +1,75 @@
+"""BASELINE configs[4] (C5) on ONE B200: R-MAT scale 28, edge factor 16
+(2^28 nodes, ~4.2 G edges after dedupe), int32 column indices, fp64 iterate.
+
+Opt-in (TPA_C5=1): the graph is generated and constructed on the GPU
+(tpa_host_graph_rmat_gpu, the host generator's streams), its out-CSR is
+downloaded for the oracle (~19 GB of host memory), and every oracle sweep
+walks 4.2 G edges on one host core (~20 s each), so the case takes minutes.
+
+Parity here (the full 116-sweep oracle preprocess would take ~45 min):
+  * the first two PageRank sweeps (cpi_run window [0, 2]) against the oracle;
+  * the stranger vector's closed-form mass ||r||_1 = (1-c)^T within eps/c
+    (SelfLoop conserves mass);
+  * two sampled queries end to end (the B = 1 path and the B = 16 batch with
+    device top-k): the oracle's family part combined with the GPU stranger
+    vector, per-vector max-abs <= 1e-12 and L1 <= 1e-9; top-10 ids equal the
+    oracle vector's top_k_nodes order.
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+import pytest
+
+import paper_1708_02574_b200 as P
+from conftest import assert_close
+
+C, EPS, S, T = 0.15, 1e-9, 5, 10
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("TPA_C5") != "1",
+                                 reason="billion-edge config: opt-in with TPA_C5=1 (minutes, ~40 GB host RAM)")]
+
+
+def _top(v, k):
+    cand = np.argpartition(-v, k + 64)[:k + 64]
+    order = np.lexsort((cand, -v[cand]))  # score desc, ties by ascending id
+    return cand[order][:k]
+
+
+def test_c5_config(oracle):
+    t0 = time.perf_counter()
+    g = P.generate_rmat(28, 16, 0.57, 0.19, 0.19, rng_seed=1, device=0)
+    n, m = g.node_count(), g.edge_count()
+    print(f"C5 graph: n={n} m={m} dangling={len(g.dangling_nodes())} in {time.perf_counter() - t0:.1f}s")
+    assert n == 1 << 28 and 3.5e9 < m < 2 ** 32
+    t0 = time.perf_counter()
+    pr2 = P.cpi_run(g, P.SeedSet.all_nodes(n), P.CpiParams(C, EPS, 0, 2))
+    print(f"C5 ingest + 2 sweeps {time.perf_counter() - t0:.1f}s, device bytes {g.device().device_bytes() / 1e9:.1f} GB")
+    t0 = time.perf_counter()
+    want2 = oracle.pagerank(g, C, EPS, 0, 2)[0]
+    print(f"oracle 2 sweeps {time.perf_counter() - t0:.1f}s")
+    assert_close(pr2.scores, want2, what="C5 pagerank window [0,2]")
+    del want2, pr2
+
+    t0 = time.perf_counter()
+    art = P.preprocess(g, C, EPS, T)
+    print(f"C5 preprocess {time.perf_counter() - t0:.2f}s")
+    st = art.stranger_scores
+    assert abs(st.sum() - (1 - C) ** T) <= EPS / C, st.sum()
+
+    seeds = P.sample_seeds(g, 16, 1)
+    t0 = time.perf_counter()
+    ids, vals = P.query_batch_topk(g, art, seeds, S, 10)
+    print(f"C5 batch of 16 + top-10 {time.perf_counter() - t0:.2f}s")
+    for k in (0, 11):
+        t0 = time.perf_counter()
+        want = oracle.query(g, st, C, EPS, T, int(seeds[k]), S)
+        print(f"oracle query {time.perf_counter() - t0:.1f}s")
+        got = P.query(g, art, int(seeds[k]), S)
+        assert_close(got, want, what=f"C5 query seed {seeds[k]}")
+        assert list(ids[k]) == list(_top(want, 10)), (k, ids[k], _top(want, 10))
+        assert np.max(np.abs(vals[k] - want[ids[k]])) <= 1e-12
+        del want, got

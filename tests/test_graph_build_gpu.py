@@ -46,3 +46,24 @@ def test_build_gpu_errors_match_reference():
         P.Graph(5, (src, dst))
     # the first offending edge in input order, the reference's message
     assert str(gpu_err.value) == str(host_err.value) == "edge endpoint out of range: 9 -> 0"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["selfloop", "drop"])
+@pytest.mark.parametrize("scale,ef,a,b,c", [(1, 1, 0.57, 0.19, 0.19), (6, 3, 0.25, 0.25, 0.25),
+                                            (12, 16, 0.57, 0.19, 0.19), (17, 16, 0.57, 0.19, 0.19)])
+def test_rmat_gpu_equals_host(policy, scale, ef, a, b, c):
+    """The GPU generator replays the host generator's per-chunk mt19937_64
+    streams (scale 17 x ef 16 = 2 chunks of 2^20 edges): same edges, same
+    graph, same fingerprint."""
+    host = P.generate_rmat(scale, ef, a, b, c, rng_seed=11, policy=policy)
+    gpu = P.generate_rmat(scale, ef, a, b, c, rng_seed=11, policy=policy, device=0)
+    _same(host, gpu)
+
+
+@pytest.mark.gpu
+def test_rmat_gpu_errors():
+    with pytest.raises(ValueError):
+        P.generate_rmat(0, 16, device=0)
+    with pytest.raises(ValueError):
+        P.generate_rmat(10, 16, 0.6, 0.3, 0.3, device=0)
