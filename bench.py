@@ -434,7 +434,9 @@ def run_ours(args):
         # dominant kernel: the SpMM sweep.  Roofline on its densest launch, the
         # last family sweep x^(S-1) (fused combine), with that sweep's exact
         # compulsory bytes; the sparse early sweeps are listed per index.
-        ver = os.environ.get("TPA_SPMM", "5") if Bk in (32, 64) else "2"
+        ver = os.environ.get("TPA_SPMM", "5") if Bk in (16, 32, 64) else "2"
+        if Bk == 16 and ver != "2":
+            ver = "5"
         kname = {"5": f"k_mm_fused<{Bk}>", "4": f"k_mm_gather<{Bk}> + k_mm_epi<{Bk}>",
                  "3": f"k_step_spmm3<{Bk}>"}.get(ver, f"k_step_spmm2<{Bk}>")
         last = per_sweep.get(S - 1)

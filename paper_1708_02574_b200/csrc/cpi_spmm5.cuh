@@ -27,12 +27,21 @@ namespace tpa {
 #define TPA_MM5_MINB 8
 #endif
 
+// B = 16 ("paired" form): a 128-byte share row is one half-warp's load, so
+// every gather instruction fetches TWO consecutive positions of the block's
+// nonzero stream (lanes 0-15 the even one, 16-31 the odd one), and a
+// shfl_xor(16) hands each half the other's value; both halves then add the
+// two terms in position order, so every lane holds its column's sum in the
+// reference's strictly sequential order (bitwise as B = 32 / 64) and the
+// halves stay in lockstep (no divergence).  32 positions per window in
+// flight per warp = 4 KB, as B = 32.
 template <int B, int RB_>
 struct Mm5 {
-    static_assert(B == 32 || B == 64, "v5: one warp per row group");
+    static_assert(B == 16 || B == 32 || B == 64, "v5: one warp per row group");
     static_assert(RB_ == 4 || RB_ == 8 || RB_ == 16, "rows per block");
-    static constexpr int CPL = B / 32;
-    static constexpr int U = 16 / CPL;         // gathers in flight per lane
+    static constexpr bool PAIR = B == 16;
+    static constexpr int CPL = PAIR ? 1 : B / 32;  // columns per lane
+    static constexpr int U = PAIR ? 32 : 16 / CPL;  // positions per gather group (PAIR: 16 loads / lane)
     static constexpr int RB = RB_;             // rows per block (the host's block window)
     static constexpr int NW = 4;               // warps per CTA
     static constexpr int NT = NW * 32;
@@ -56,6 +65,7 @@ template <int B, bool kLast, int RB>
 __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Args P) {
     using Sh = Mm5<B, RB>;
     constexpr int CPL = Sh::CPL, U = Sh::U, TS = Sh::TS;
+    constexpr bool PAIR = Sh::PAIR;
     const MmArgs& A = P.m;
     const StepArgs& a = A.s;
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -64,7 +74,8 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int c0 = lane * CPL;
+    const int c0 = PAIR ? (lane & 15) : lane * CPL;
+    const int half = lane >> 4;  // PAIR: which position of a pair this lane loads
     double (*yb)[B] = reinterpret_cast<double (*)[B]>(s_dyn + (size_t)wid * Sh::kWarpBytes);
     double* tile = reinterpret_cast<double*>(s_dyn + (size_t)wid * Sh::kWarpBytes + Sh::kYBytes);
 
@@ -198,10 +209,52 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 for (int h = 0; h < 32 / U; ++h) {
                     const int64_t base = wbase + h * U;
                     if (base >= e1) break;  // warp-uniform
-                    const uint32_t lmask = (live32 >> (h * U)) & ((1u << U) - 1u);
+                    const uint32_t lmask = U == 32 ? live32 : (live32 >> (h * U)) & ((1u << (U & 31)) - 1u);
                     const int64_t p = rpl - base;
                     const uint32_t smask = __ballot_sync(0xffffffffu, starts && p >= 0 && p < U);
-                    if (lmask) {
+                    if (PAIR && lmask) {
+                        // 16 loads per lane: position 2*jp + half of the window
+                        double v[U / 2];
+#pragma unroll
+                        for (int jp = 0; jp < U / 2; ++jp) {
+                            const int pp = 2 * jp + half;
+                            const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + pp);
+                            v[jp] = ((lmask >> pp) & 1u) ? __ldg(share + (size_t)u * B + c0) : 0.0;
+                        }
+                        // the term of position j (both halves, in order)
+                        double od = 0.0;
+                        auto term = [&](int j) -> double {
+                            if (j & 1) return od;
+                            const double x = v[j >> 1];
+                            const double y = __shfl_xor_sync(0xffffffffu, x, 16);
+                            od = half ? x : y;
+                            return half ? y : x;
+                        };
+                        if (smask == 0) {
+#pragma unroll
+                            for (int j = 0; j < U; ++j) s[0] = dadd(s[0], term(j));
+                        } else {
+                            uint32_t m = smask;
+                            int k_next = __ffs(m) - 1;
+                            m &= m - 1;
+                            int pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
+#pragma unroll
+                            for (int j = 0; j < U; ++j) {
+                                const double t = term(j);
+                                if (j == pos_next) {  // warp-uniform
+                                    close_row(k_next);
+                                    if (m) {
+                                        k_next = __ffs(m) - 1;
+                                        m &= m - 1;
+                                        pos_next = (int)__shfl_sync(0xffffffffu, p, k_next);
+                                    } else {
+                                        pos_next = U;
+                                    }
+                                }
+                                s[0] = dadd(s[0], t);
+                            }
+                        }
+                    } else if (!PAIR && lmask) {
                         double v[U][CPL];
 #pragma unroll
                         for (int j = 0; j < U; ++j) {
@@ -363,6 +416,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int b = c0 + c;
+        if (PAIR && half) break;  // the upper half-warp mirrors the lower one's columns
         if (fx[0][c] | fx[1][c]) fx_atomic_add(&s_fx[4 * b + 0], &s_fx[4 * b + 1], fx[0][c], fx[1][c]);
         if (fx[2][c] | fx[3][c]) fx_atomic_add(&s_fx[4 * b + 2], &s_fx[4 * b + 3], fx[2][c], fx[3][c]);
     }

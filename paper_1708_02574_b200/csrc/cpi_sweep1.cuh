@@ -38,17 +38,16 @@ __global__ void __launch_bounds__(256) k_s1_rows(Sweep1Args P) {
     if (!a.state_in[b].active) return;
     const uint32_t seed = P.seeds.s[b];
     const uint64_t lo = __ldg(P.out_off + seed), hi = __ldg(P.out_off + seed + 1);
-    // one row per warp: 32 lanes x CPL columns
-    constexpr int CPL = B / 32;
+    // one row per warp: the lanes cover the B columns
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (uint64_t e = lo + blockIdx.x * (blockDim.x / 32) + w; e < hi; e += gridDim.x * (blockDim.x / 32)) {
         const uint32_t v = __ldg(P.out_tgt + e);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) a.share_out[(size_t)v * B + lane * CPL + c] = 0.0;
+        for (int c = lane; c < B; c += 32) a.share_out[(size_t)v * B + c] = 0.0;
         const bool valid = (__ldcg(P.acc_valid + (v >> 5)) >> (v & 31)) & 1u;
         if (!valid) {
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) a.acc[(size_t)v * B + lane * CPL + c] = 0.0;
+            for (int c = lane; c < B; c += 32) a.acc[(size_t)v * B + c] = 0.0;
             __syncwarp();
             if (lane == 0) atomicOr(P.acc_valid + (v >> 5), 1u << (v & 31));
         }

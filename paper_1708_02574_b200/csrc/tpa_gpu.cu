@@ -343,6 +343,7 @@ static int spmm_version(int B) {
         const char* e = std::getenv("TPA_SPMM");
         return e ? std::atoi(e) : 5;
     }();
+    if (B == 16) return env == 2 ? 2 : 5;  // v5 paired half-warps (TPA_SPMM=2: the v2 kernel)
     if (B != 32 && B != 64) return 2;
     return (env >= 2 && env <= 4) ? env : 5;
 }
@@ -756,7 +757,10 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                           g->out_tgt.as<uint32_t>(), *push_seeds, mm->nz_out, mm->acc_valid,
                           w.s1_skip.as<uint32_t>()};
             const dim3 g1(8, B);  // 8 chunks per column: a hub seed's out-list is spread
-            if (B == 32) {
+            if (B == 16) {
+                k_s1_rows<16><<<g1, 256, 0, g->stream>>>(S1);
+                k_s1_push<16><<<g1, 256, 0, g->stream>>>(S1);
+            } else if (B == 32) {
                 k_s1_rows<32><<<g1, 256, 0, g->stream>>>(S1);
                 k_s1_push<32><<<g1, 256, 0, g->stream>>>(S1);
             } else {
@@ -809,7 +813,10 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             g->launches -= 1;  // no pull this sweep: cancels the common ++ below
         } else if (spmm_version(B) == 5) {
             const bool last = a.out != nullptr;
-            if (B == 32) {
+            if (B == 16) {
+                if (last) launch_fused_rb<16, true>(P, rb, g->num_sms, g->stream);
+                else launch_fused_rb<16, false>(P, rb, g->num_sms, g->stream);
+            } else if (B == 32) {
                 if (last) launch_fused_rb<32, true>(P, rb, g->num_sms, g->stream);
                 else launch_fused_rb<32, false>(P, rb, g->num_sms, g->stream);
             } else {

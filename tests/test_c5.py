@@ -44,7 +44,9 @@ def test_c5_config(oracle):
     g = P.generate_rmat(28, 16, 0.57, 0.19, 0.19, rng_seed=1, device=0)
     n, m = g.node_count(), g.edge_count()
     print(f"C5 graph: n={n} m={m} dangling={len(g.dangling_nodes())} in {time.perf_counter() - t0:.1f}s")
-    assert n == 1 << 28 and 3.5e9 < m < 2 ** 32
+    # m counts the SelfLoop repair edges of the dangling nodes: above 2^32 (64-bit
+    # edge offsets everywhere, 32-bit column indices)
+    assert n == 1 << 28 and 3.5e9 < m < 2 ** 32 + n
     t0 = time.perf_counter()
     pr2 = P.cpi_run(g, P.SeedSet.all_nodes(n), P.CpiParams(C, EPS, 0, 2))
     print(f"C5 ingest + 2 sweeps {time.perf_counter() - t0:.1f}s, device bytes {g.device().device_bytes() / 1e9:.1f} GB")
