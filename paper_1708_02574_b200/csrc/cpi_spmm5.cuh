@@ -23,6 +23,14 @@ namespace tpa {
 #ifndef TPA_EPI_STORE_HINT
 #define TPA_EPI_STORE_HINT 0
 #endif
+// A/B knobs: an unpredicated gather group when all its sources are live;
+// the window's gather groups unrolled (shuffle lanes become immediates).
+#ifndef TPA_MM5_ALL_LIVE
+#define TPA_MM5_ALL_LIVE 0
+#endif
+#ifndef TPA_MM5_UNROLL_H
+#define TPA_MM5_UNROLL_H 0
+#endif
 #ifndef TPA_MM5_MINB
 #define TPA_MM5_MINB 8
 #endif
@@ -162,7 +170,8 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         const uint32_t av = (A.acc_valid && a.acc) ? __ldcg(A.acc_valid + (r0 >> 5)) : 0u;
         const uint32_t dl = lane < nrows ? __ldg(a.deg + r0 + lane) : 0u;
         if (!is_seg && a.acc) {
-            for (int k = 0; k < nrows; ++k)
+            // PAIR: each half-warp fetches the rows its epilogue takes
+            for (int k = PAIR ? half : 0; k < nrows; k += PAIR ? 2 : 1)
                 if ((av >> ((r0 + k) & 31)) & 1u)
                     cp_async_acc<CPL>(tile + k * TS + c0, a.acc + (size_t)(r0 + k) * B + c0);
         }
@@ -180,10 +189,14 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         for (int k = 0; k < nrows; ++k)
 #pragma unroll
             for (int c = 0; c < CPL; ++c) yb[k][c0 + c] = 0.0;
+        // PAIR: only the lower half-warp's sums are in position order (the
+        // upper half adds the same two terms the other way round), so only
+        // the lower half stores them
+        const bool keeper = !PAIR || half == 0;
         auto close_row = [&](int k_next) {
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                yb[cur][c0 + c] = s[c];
+                if (keeper) yb[cur][c0 + c] = s[c];
                 s[c] = 0.0;
             }
             cur = k_next;
@@ -205,7 +218,11 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 const uint32_t w1 = bits32(i1, wbase + 32);
                 const uint32_t live32 =
                     __ballot_sync(0xffffffffu, ((w0 >> (i0 & 31)) & 1u) && wbase + lane < e1);
+#if TPA_MM5_UNROLL_H
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
                 for (int h = 0; h < 32 / U; ++h) {
                     const int64_t base = wbase + h * U;
                     if (base >= e1) break;  // warp-uniform
@@ -221,14 +238,15 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                             const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + pp);
                             v[jp] = ((lmask >> pp) & 1u) ? __ldg(share + (size_t)u * B + c0) : 0.0;
                         }
-                        // the term of position j (both halves, in order)
+                        // the term of position j: the lower half holds 2j'
+                        // and receives 2j'+1 from the upper half, so its sum
+                        // runs in position order (the upper half's is unused)
                         double od = 0.0;
                         auto term = [&](int j) -> double {
                             if (j & 1) return od;
                             const double x = v[j >> 1];
-                            const double y = __shfl_xor_sync(0xffffffffu, x, 16);
-                            od = half ? x : y;
-                            return half ? y : x;
+                            od = __shfl_xor_sync(0xffffffffu, x, 16);
+                            return x;
                         };
                         if (smask == 0) {
 #pragma unroll
@@ -256,14 +274,24 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                         }
                     } else if (!PAIR && lmask) {
                         double v[U][CPL];
+                        if (TPA_MM5_ALL_LIVE && lmask == (U == 32 ? 0xffffffffu : (1u << (U & 31)) - 1u)) {
+                            // every source of the group is live (dense sweeps): no
+                            // per-load predicates or zero fills
 #pragma unroll
-                        for (int j = 0; j < U; ++j) {
-                            const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
-                            if ((lmask >> j) & 1u) {
+                            for (int j = 0; j < U; ++j) {
+                                const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
                                 ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
-                            } else {
+                            }
+                        } else {
 #pragma unroll
-                                for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
+                            for (int j = 0; j < U; ++j) {
+                                const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
+                                if ((lmask >> j) & 1u) {
+                                    ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
+                                } else {
+#pragma unroll
+                                    for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
+                                }
                             }
                         }
                         if (smask == 0) {
@@ -312,7 +340,8 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         if (is_seg) {
             // publish the segment; the last one of the row combines in order
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) A.seg_part[(size_t)item * B + c0 + c] = s[c];
+            for (int c = 0; c < CPL; ++c)
+                if (keeper) A.seg_part[(size_t)item * B + c0 + c] = s[c];
             __threadfence();
             __syncwarp();
             const uint32_t li = A.seg_long[item];
@@ -332,7 +361,8 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         } else if (ne_mask) {
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) yb[cur][c0 + c] = s[c];
+            for (int c = 0; c < CPL; ++c)
+                if (keeper) yb[cur][c0 + c] = s[c];
         }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
@@ -342,22 +372,27 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
 #pragma unroll
         for (int c = 0; c < CPL; ++c) bl1[c] = bdm[c] = 0.0;
         uint32_t nzw = 0, avw = 0;
-        for (int k = 0; k < nrows; ++k) {
+        // PAIR: the half-warps take alternate rows (16 lanes = 16 columns each)
+        constexpr int KS = PAIR ? 2 : 1;
+        const uint32_t hmask = PAIR ? (0xffffu << (16 * half)) : 0xffffffffu;
+        for (int k0 = 0; k0 < nrows; k0 += KS) {
+            const int k = k0 + (PAIR ? half : 0);
+            const bool kin = k < nrows;
             const uint32_t r = r0 + k;
-            const bool valid = (av >> (r & 31)) & 1u;
+            const uint32_t d = __shfl_sync(0xffffffffu, dl, kin ? k : 0);
+            const bool valid = kin && ((av >> (r & 31)) & 1u);
             double yy[CPL], ao[CPL];
             bool nzc = false;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                yy[c] = yb[k][c0 + c];
+                yy[c] = kin ? yb[k][c0 + c] : 0.0;
                 if (st[c].has_spread) yy[c] = dadd(yy[c], st[c].spread);  // graph.cpp:265-268
                 if (!st[c].active) yy[c] = 0.0;
                 ao[c] = valid ? tile[k * TS + c0 + c] : 0.0;
                 nzc = nzc || yy[c] != 0.0;
             }
-            const bool row_nz = __any_sync(0xffffffffu, nzc);
-            if (!kLast && !row_nz) continue;  // nothing changes for this row
-            const uint32_t d = __shfl_sync(0xffffffffu, dl, k);
+            const bool row_nz = (__ballot_sync(0xffffffffu, nzc) & hmask) != 0;
+            if (!kin || (!kLast && !row_nz)) continue;  // nothing changes for this row
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 const size_t ix = (size_t)r * B + c0 + c;
@@ -384,6 +419,10 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             }
             nzw |= (row_nz ? 1u : 0u) << (r & 31);
             avw |= 1u << (r & 31);
+        }
+        if (PAIR) {
+            nzw |= __shfl_xor_sync(0xffffffffu, nzw, 16);
+            avw |= __shfl_xor_sync(0xffffffffu, avw, 16);
         }
         if (kLast) {
             __syncwarp();
@@ -416,7 +455,6 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int b = c0 + c;
-        if (PAIR && half) break;  // the upper half-warp mirrors the lower one's columns
         if (fx[0][c] | fx[1][c]) fx_atomic_add(&s_fx[4 * b + 0], &s_fx[4 * b + 1], fx[0][c], fx[1][c]);
         if (fx[2][c] | fx[3][c]) fx_atomic_add(&s_fx[4 * b + 2], &s_fx[4 * b + 3], fx[2][c], fx[3][c]);
     }

@@ -68,9 +68,16 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
     return s;
 }
 
+// kRowFx = false: the residual / dangling mass as per-tile fixed-tree double
+// sums, added across tiles in exact fixed point (the totals depend on the
+// tiling only; a row partition cuts at tile starts, tpa_part.cuh).
+// kRowFx = true (the relabelled twin, tpa_relabel.cuh): every row's |y| goes
+// into exact fixed point on its own, so any tiling gives the same totals.
 #ifdef TPA_MV2_MINB  // A/B knob; the default (no minimum) compiles to 40 registers, 6 CTAs/SM
+template <bool kRowFx>
 __global__ void __launch_bounds__(kThreads, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
 #else
+template <bool kRowFx>
 __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
 #endif
     const StepArgs& a = M.s;
@@ -104,7 +111,22 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         return;
     }
     const bool want_dm = a.policy == kUniform;
+    // |y| and the dangling mass go into exact 128-bit fixed point ROW BY ROW:
+    // the totals are then independent of how rows are grouped into tiles (a
+    // row partition, or the relabelled twin of tpa_relabel.cuh, reproduces
+    // them bit for bit)
+    unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+    __shared__ unsigned long long s_w[4 * (kThreads / 32)];
     double my_l1 = 0.0, my_dm = 0.0;
+    auto add_row = [&](double y, bool dangling) {
+        if constexpr (kRowFx) {
+            fx_add(f0, f1, y);
+            if (want_dm && dangling) fx_add(f2, f3, y);
+        } else {
+            my_l1 = dadd(my_l1, fabs(y));
+            if (want_dm && dangling) my_dm = dadd(my_dm, y);
+        }
+    };
 
     if (!is_long) {
         const uint32_t nrows = re - rb;
@@ -188,8 +210,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
                 a.share_out[vtx] = sv;
                 for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][vtx] = sv;
             }
-            my_l1 = dadd(my_l1, fabs(y));
-            if (want_dm && dg[q] == 0) my_dm = dadd(my_dm, y);
+            add_row(y, dg[q] == 0);
         }
     } else {
         // one long row: every thread sums a fixed strided subset, then a fixed tree
@@ -213,24 +234,30 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
             const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
             if (a.share_out)
                 for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][rb] = d ? ddiv(dmul(a.keep, y), (double)d) : 0.0;
-            my_l1 = fabs(y);
-            if (want_dm && d == 0) my_dm = y;
+            add_row(y, d == 0);
         }
     }
-    // tile partials (fixed tree) -> exact fixed-point totals across tiles
-    const double tl1 = block_sum(my_l1, s_red);
-    const double tdm = want_dm ? block_sum(my_dm, s_red) : 0.0;
+    if constexpr (kRowFx) {
+        // exact CTA totals -> the sweep's totals (order-free integer sums)
+        fx_cta_flush(f0, f1, f2, f3, s_w, M.fx);
+    } else {
+        // tile partials (fixed tree) -> exact fixed-point totals across tiles
+        const double tl1 = block_sum(my_l1, s_red);
+        const double tdm = want_dm ? block_sum(my_dm, s_red) : 0.0;
+        if (tid == 0) {
+            unsigned long long h = 0, l = 0;
+            if (tl1 != 0.0) {
+                fx_add(h, l, tl1);
+                fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
+            }
+            if (tdm != 0.0) {
+                h = l = 0;
+                fx_add(h, l, tdm);
+                fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
+            }
+        }
+    }
     if (tid == 0) {
-        unsigned long long h = 0, l = 0;
-        if (tl1 != 0.0) {
-            fx_add(h, l, tl1);
-            fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
-        }
-        if (tdm != 0.0) {
-            h = l = 0;
-            fx_add(h, l, tdm);
-            fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
-        }
         __threadfence();
         s_ticket = atomicAdd(a.done_cnt, 1u);
     }

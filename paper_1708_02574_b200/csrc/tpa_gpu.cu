@@ -9,6 +9,7 @@
 // Per-width workspace (B = 1, 8, 16, 32, 64): share ping-pong [n][B] fp64,
 // acc [n][B] fp64, reduction partials, ticket counters, ColState x2.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <nccl.h>
 
 #include <algorithm>
@@ -364,6 +365,7 @@ static int mm5_rows(int B, uint32_t step) {
         return e ? (uint32_t)std::atoi(e) : 0u;
     }();
     if (B == 32) return step <= wide_steps ? 16 : 8;
+    if (B == 16) return 16;  // 2.2 KB of shared memory per warp either way: 1.23 -> 1.13 ms per C2 batch
     return 8;
 }
 
@@ -438,6 +440,14 @@ static int mm_occupancy() {
     return occ;
 }
 
+// The CSR(Ãᵀ) of the graph with nodes numbered by out-degree (tpa_relabel.cuh).
+struct Relabel {
+    DevBuf row_ptr, col, deg;  // twin CSR(Ãᵀ) and out-degrees, new ids
+    DevBuf perm;               // perm[new id] = old id
+    DevBuf acc;                // window accumulator in new-id order
+    Schedule mv;               // SpMV tiles of the twin
+};
+
 struct Workspace {
     int B = 0;
     DevBuf share[2], acc, part, gpart, group_cnt, done_cnt, state;
@@ -504,6 +514,7 @@ struct tpa_graph {
     DevBuf row_ptr, col, deg;
     DevBuf out_off, out_tgt;  // the out-edge CSR itself (frontier push-marking)
     Schedule mv;  // SpMV work items
+    std::unique_ptr<Relabel> rl;  // relabelled twin for dense-start B = 1 runs (tpa_relabel.cuh), built lazily
     LongRows longs;
     uint32_t n_blocks = 0;  // kMmRows-row blocks
     std::map<int, std::unique_ptr<Workspace>> ws;
@@ -728,8 +739,8 @@ static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
 }
 
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
-                        const SeedList* push_seeds = nullptr) {
-    const Schedule& s = g->mv;
+                        const SeedList* push_seeds = nullptr, const Schedule* sched = nullptr) {
+    const Schedule& s = sched ? *sched : g->mv;
     const dim3 grid(B == 1 ? s.n_items : (uint32_t)w.grid), block(kThreads);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g->profile) {
@@ -854,23 +865,33 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             {
                 static const bool carve = [] {  // A/B: shared-memory carveout (L1 share) for v2
                     const char* e = std::getenv("TPA_MV_CARVEOUT");
-                    if (e) CK(cudaFuncSetAttribute(k_step_spmv2, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
+                    if (e) CK(cudaFuncSetAttribute(k_step_spmv2<false>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
                     return e != nullptr;
                 }();
                 (void)carve;
-                MvArgs M{a, g->mv.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
+                MvArgs M{a, s.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
                          !g->part ? nullptr
                          : a.share_out ? reinterpret_cast<unsigned long long*>(a.share_out + g->part->slice)
                                        : w.limbs.as<unsigned long long>() + (a.step & 1) * 6,
                          PeerOut{}, g->part ? g->part->slice : 0u};
                 if (g->part && a.share_out) M.peers = g->peer_out;
                 static const bool smem_ok = [] {
-                    CK(cudaFuncSetAttribute(k_step_spmv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    CK(cudaFuncSetAttribute(k_step_spmv2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)kMvDynSmem));
                     return true;
                 }();
                 (void)smem_ok;
-                k_step_spmv2<<<grid, block, kMvDynSmem, g->stream>>>(M);
+                if (sched && sched != &g->mv) {  // the relabelled twin: per-row exact totals
+                    static const bool smem_rf = [] {
+                        CK(cudaFuncSetAttribute(k_step_spmv2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)kMvDynSmem));
+                        return true;
+                    }();
+                    (void)smem_rf;
+                    k_step_spmv2<true><<<grid, block, kMvDynSmem, g->stream>>>(M);
+                } else {
+                    k_step_spmv2<false><<<grid, block, kMvDynSmem, g->stream>>>(M);
+                }
             }
             else
             {
@@ -911,6 +932,8 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
 // per-column state (cpi.cpp:70-81) advances on the device.  Only a run to
 // convergence (terminal < 0) checks the state on the host after the
 // estimated horizon, and continues if a column is still active.
+#include "tpa_relabel.cuh"
+
 static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int B = cfg.B;
     Workspace& w = g->workspace(B);
@@ -923,6 +946,22 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const double keep = 1.0 - cfg.c;
     ColState* st = w.state.as<ColState>();
     const bool partition = !cfg.bounds.empty() || !cfg.seg_acc.empty();
+    // dense-start B = 1 runs sweep the relabelled twin (tpa_relabel.cuh): the
+    // same additions in the same order, hub shares packed into few lines
+    Relabel* rl = (B == 1 && !partition && !cfg.y_out && !cfg.out && cfg.init == Init::Dense && !cfg.d_x &&
+                   spmv_version() == 2)
+                      ? relabel_view(g)
+                      : nullptr;
+    double* acc_run = cfg.acc;
+    if (rl && cfg.acc) {
+        if (cfg.acc != w.acc.as<double>()) {
+            acc_run = w.acc.as<double>();
+        } else {
+            rl->acc.ensure((size_t)n * 8, g->stream);
+            acc_run = rl->acc.as<double>();
+        }
+    }
+    const uint32_t* const deg_run = rl ? rl->deg.as<uint32_t>() : g->deg.as<uint32_t>();
 
     // accumulator for x⁽⁰⁾, zero the rest
     double* acc0 = nullptr;
@@ -935,16 +974,16 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     } else if (cfg.acc && mm) {
         acc0 = cfg.acc;  // validity tracked by acc_valid
         CK(cudaMemsetAsync(w.acc_valid.p, 0, bm_bytes, g->stream));
-    } else if (cfg.acc) {
+    } else if (acc_run) {
         const bool in0 = cfg.start == 0;
         if (!in0 || cfg.init == Init::Seeds)
-            CK(cudaMemsetAsync(cfg.acc, 0, (size_t)n * B * 8, g->stream));
-        acc0 = in0 ? cfg.acc : nullptr;
+            CK(cudaMemsetAsync(acc_run, 0, (size_t)n * B * 8, g->stream));
+        acc0 = in0 ? acc_run : nullptr;
     }
     const int active0 = cfg.terminal != 0;
     if (cfg.init == Init::Dense) {
         const int nblk = grid_for(n, 4 * kThreads, 4 * g->num_sms);
-        k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.d_x, cfg.weight, n, g->deg.as<uint32_t>(), keep,
+        k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.d_x, cfg.weight, n, deg_run, keep,
                                                        w.share[0].as<double>(), acc0,
                                                        w.fx.as<unsigned long long>());
         CKL("k_init_dense");
@@ -971,11 +1010,12 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     }
 
     StepArgs a{};
-    a.row_ptr = g->row_ptr.as<int64_t>();
-    a.col = g->col.as<uint32_t>();
-    a.deg = g->deg.as<uint32_t>();
-    a.items = sch.items.as<uint2>();
-    a.n_items = sch.n_items;
+    const Schedule& sch_run = rl ? rl->mv : sch;
+    a.row_ptr = rl ? rl->row_ptr.as<int64_t>() : g->row_ptr.as<int64_t>();
+    a.col = rl ? rl->col.as<uint32_t>() : g->col.as<uint32_t>();
+    a.deg = deg_run;
+    a.items = sch_run.items.as<uint2>();
+    a.n_items = sch_run.n_items;
     a.n = n;
     a.policy = g->policy;
     a.keep = keep;
@@ -1025,7 +1065,7 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
                 a.acc = cfg.seg_acc[seg_of(cfg.bounds, i)];
             } else {
                 const bool inw = i >= cfg.start && (cfg.terminal < 0 || (int64_t)i <= cfg.terminal);
-                a.acc = inw ? cfg.acc : nullptr;
+                a.acc = inw ? acc_run : nullptr;
             }
             a.out = (last && cfg.out) ? cfg.out : nullptr;
             combined = combined || a.out != nullptr;
@@ -1041,7 +1081,7 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             // element) instead of a pull over every nonzero
             const bool s1 = mm && i == 1 && cfg.init == Init::Seeds && a.acc && a.share_out && !a.out &&
                             !cfg.y_out && g->policy != kUniform && spmm_version(B) == 5 && !g->s1_push_off;
-            launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr);
+            launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr, &sch_run);
         }
         done += chunk;
         if ((int64_t)done >= target) break;
@@ -1059,6 +1099,12 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             acc_final, mm ? w.acc_valid.as<uint32_t>() : nullptr, n, B, cfg.b_valid, cfg.stranger, cfg.scale,
             cfg.node_major ? 1 : 0, cfg.out);
         CKL("k_combine");
+        ++g->launches;
+    }
+    if (rl && cfg.acc) {  // the window accumulator back in original ids
+        k_rl_unpermute<<<grid_for(n, 256, 8 * g->num_sms), 256, 0, g->stream>>>(acc_run, rl->perm.as<uint32_t>(), n,
+                                                                                  cfg.acc);
+        CKL("k_rl_unpermute");
         ++g->launches;
     }
     if (res && cfg.want_state) {
@@ -1382,6 +1428,7 @@ int tpa_graph_destroy(tpa_graph* g) {
             DeviceGuard dg(g->device);
             // stream-ordered frees first, then drain and drop the stream
             g->ws.clear();
+            g->rl.reset();
             g->row_ptr.release();
             g->col.release();
             g->deg.release();
@@ -1455,7 +1502,9 @@ int tpa_graph_info(const tpa_graph* g, uint32_t* n, uint64_t* m, uint64_t* finge
         if (fingerprint) *fingerprint = g->fingerprint;
         if (policy) *policy = g->policy;
         if (device_bytes) {
-            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->longs.seg_lo.bytes * 2;
+            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->longs.seg_lo.bytes * 2 +
+                         g->out_off.bytes + g->out_tgt.bytes;
+            if (g->rl) b += g->rl->row_ptr.bytes + g->rl->col.bytes + g->rl->deg.bytes + g->rl->perm.bytes + g->rl->acc.bytes;
             for (auto& kv : g->ws) {
                 const Workspace& w = *kv.second;
                 b += w.share[0].bytes + w.share[1].bytes + w.acc.bytes + w.part.bytes + w.gpart.bytes;

@@ -348,8 +348,11 @@ __global__ void k_seg_offsets(int* off, uint32_t B, uint32_t k) {
 }
 
 // top-k of B device-resident vectors [B][n] into device ids / scores [B][k].
+// `scratch` (optional, >= B * n * 4 bytes): a dead device buffer to hold the
+// candidate lists instead of the handle's own (the query path passes the
+// batch's accumulator, free once its last sweep has combined).
 static void topk_device(tpa_graph* g, const double* scores, uint32_t B, uint32_t k, uint32_t* d_ids,
-                        double* d_scores) {
+                        double* d_scores, void* scratch = nullptr, size_t scratch_bytes = 0) {
     cudaStream_t s = g->stream;
     const uint32_t n = g->n;
     auto& W = g->topk;
@@ -359,10 +362,16 @@ static void topk_device(tpa_graph* g, const double* scores, uint32_t B, uint32_t
         hist.ensure((size_t)B * kTkBins * 4, g->stream);
         CK(cudaMemsetAsync(hist.p, 0, hist.bytes, s));  // the selects leave it zeroed
     }
-    cand.ensure((size_t)B * n * 4, g->stream);
+    uint32_t* cand_p = nullptr;
+    if (scratch && scratch_bytes >= (size_t)B * n * 4) {
+        cand_p = static_cast<uint32_t*>(scratch);
+    } else {
+        cand.ensure((size_t)B * n * 4, g->stream);
+        cand_p = cand.as<uint32_t>();
+    }
     ids.ensure((size_t)B * k * 4, g->stream);
     k_topk_init<<<(B + 127) / 128, 128, 0, s>>>(st.as<TopkState>(), B, k);
-    TkArgs A{scores, n, k, st.as<TopkState>(), hist.as<uint32_t>(), cand.as<uint32_t>(), ids.as<uint32_t>()};
+    TkArgs A{scores, n, k, st.as<TopkState>(), hist.as<uint32_t>(), cand_p, ids.as<uint32_t>()};
     // a few CTAs per vector, each over >= 16k elements: the per-CTA histogram
     // zeroing / flushing (4096 bins) must stay small against the scan
     const uint32_t full_x = (uint32_t)grid_for(n, 256 * 64, std::max(1, (int)(8 * g->num_sms / std::max<uint32_t>(B, 1))));
@@ -490,7 +499,7 @@ int tpa_query_batch_topk(tpa_graph* g, const tpa_artifact* a, const uint32_t* se
                            scale, true, scores, TPA_DEVICE_PTRS | TPA_ASYNC);
             uint32_t* d_ids = dev ? out_ids + (size_t)b0 * k : ids.as<uint32_t>();
             double* d_sc = out_scores ? (dev ? out_scores + (size_t)b0 * k : sc.as<double>()) : nullptr;
-            topk_device(g, scores, bv, k, d_ids, d_sc);
+            topk_device(g, scores, bv, k, d_ids, d_sc, w.acc.p, w.acc.bytes);  // acc is dead until the next init
             if (!dev) {
                 download(g, out_ids + (size_t)b0 * k, ids.p, (size_t)bv * k * 4);
                 if (out_scores) download(g, out_scores + (size_t)b0 * k, sc.p, (size_t)bv * k * 8);
