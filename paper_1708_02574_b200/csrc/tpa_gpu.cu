@@ -952,6 +952,19 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
                    spmv_version() == 2)
                       ? relabel_view(g)
                       : nullptr;
+    // A/B (with the twin): TPA_L2_PERSIST_MB of the share vector's hottest
+    // (lowest twin id) entries marked L2-persisting for the sweeps
+    static const size_t rl_persist_env = [] {
+        const char* e = std::getenv("TPA_L2_PERSIST_MB");
+        return e ? (size_t)std::atoi(e) << 20 : (size_t)0;
+    }();
+    const size_t rl_persist = rl ? rl_persist_env : 0;
+    if (rl_persist) {
+        int dev = 0, mx = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)mx, rl_persist)));
+    }
     double* acc_run = cfg.acc;
     if (rl && cfg.acc) {
         if (cfg.acc != w.acc.as<double>()) {
@@ -1081,6 +1094,15 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             // element) instead of a pull over every nonzero
             const bool s1 = mm && i == 1 && cfg.init == Init::Seeds && a.acc && a.share_out && !a.out &&
                             !cfg.y_out && g->policy != kUniform && spmm_version(B) == 5 && !g->s1_push_off;
+            if (rl && rl_persist) {  // the hub shares (the twin's first ids) persist in L2
+                cudaStreamAttrValue av{};
+                av.accessPolicyWindow.base_ptr = const_cast<double*>(a.share_in);
+                av.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)n * 8, rl_persist);
+                av.accessPolicyWindow.hitRatio = 1.0f;
+                av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+            }
             launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr, &sch_run);
         }
         done += chunk;
@@ -1100,6 +1122,12 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             cfg.node_major ? 1 : 0, cfg.out);
         CKL("k_combine");
         ++g->launches;
+    }
+    if (rl_persist) {
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.num_bytes = 0;
+        CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+        CK(cudaCtxResetPersistingL2Cache());
     }
     if (rl && cfg.acc) {  // the window accumulator back in original ids
         k_rl_unpermute<<<grid_for(n, 256, 8 * g->num_sms), 256, 0, g->stream>>>(acc_run, rl->perm.as<uint32_t>(), n,
@@ -1367,6 +1395,12 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
             CK(cudaDeviceGetDefaultMemPool(&pool, device));
             uint64_t thr = UINT64_MAX;
             CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
+        if (const char* e = std::getenv("TPA_L2_FETCH")) {  // A/B: L2 fetch granularity for DRAM misses (bytes)
+            CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(e)));
+            size_t v = 0;
+            CK(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
+            if (std::getenv("TPA_DEBUG")) fprintf(stderr, "tpa: L2 fetch granularity %zu\n", v);
         }
 
         DevBuf d_off, d_tgt, d_src, d_keys;
