@@ -243,6 +243,7 @@ __device__ __forceinline__ void combine_only(const StepArgs& a, uint32_t v, uint
 // One CTA per work item: a tile of consecutive short rows (<= kMvTileNnz nnz)
 // staged through shared memory, or one long row reduced by the whole CTA.
 // ---------------------------------------------------------------------------
+constexpr size_t kMv1DynSmem = (size_t)kMvTileNnz * 8 + (kMvTileRows + 1) * 8 + (size_t)kMvTileRows * 8;
 __global__ void __launch_bounds__(kThreads) k_step_spmv(StepArgs a) {
     extern __shared__ __align__(16) unsigned char s_mv1[];  // kMvTileNnz + 2 kMvTileRows + 1 words
     double* s_vals = reinterpret_cast<double*>(s_mv1);

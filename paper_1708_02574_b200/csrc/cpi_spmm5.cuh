@@ -31,6 +31,9 @@ namespace tpa {
 #ifndef TPA_MM5_UNROLL_H
 #define TPA_MM5_UNROLL_H 0
 #endif
+#ifndef TPA_MM5_SLIM
+#define TPA_MM5_SLIM 0
+#endif
 #ifndef TPA_MM5_MINB
 #define TPA_MM5_MINB 8
 #endif
@@ -77,8 +80,15 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     const MmArgs& A = P.m;
     const StepArgs& a = A.s;
     extern __shared__ __align__(16) unsigned char s_dyn[];
+#if TPA_MM5_SLIM
+    // column states read straight from global memory and the CTA's
+    // fixed-point totals aliased onto the (by then idle) dynamic tile:
+    // 2 KB less static shared memory per CTA, left to the L1
+    unsigned long long* s_fx = reinterpret_cast<unsigned long long*>(s_dyn);
+#else
     __shared__ ColState s_st[B];
     __shared__ unsigned long long s_fx[4 * B];
+#endif
     __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -87,14 +97,20 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     double (*yb)[B] = reinterpret_cast<double (*)[B]>(s_dyn + (size_t)wid * Sh::kWarpBytes);
     double* tile = reinterpret_cast<double*>(s_dyn + (size_t)wid * Sh::kWarpBytes + Sh::kYBytes);
 
+#if !TPA_MM5_SLIM
     for (int i = tid; i < 4 * B; i += Sh::NT) s_fx[i] = 0ull;
     for (int b = tid; b < B; b += Sh::NT) s_st[b] = a.state_in[b];
+#endif
     __syncthreads();
     ColState st[CPL];
     bool any_active = false;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
+#if TPA_MM5_SLIM
+        st[c] = a.state_in[c0 + c];
+#else
         st[c] = s_st[c0 + c];
+#endif
         any_active = any_active || st[c].active;
     }
     any_active = __any_sync(0xffffffffu, any_active);
@@ -452,6 +468,11 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     }
 
     // residual / dangling mass: exact integer sums; the last CTA advances state
+#if TPA_MM5_SLIM
+    __syncthreads();  // every warp is done with its tile: s_fx may overlay it
+    for (int i = tid; i < 4 * B; i += Sh::NT) s_fx[i] = 0ull;
+    __syncthreads();
+#endif
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int b = c0 + c;

@@ -29,7 +29,15 @@ struct PeerOut {
     uint32_t n;
 };
 
-constexpr size_t kMvDynSmem = (size_t)kMvTileNnz * 8 + (kMvTileRows + 1) * 8 + (size_t)kMvTileRows * 8;
+#ifndef TPA_MV2_SEGSCAN
+#define TPA_MV2_SEGSCAN 0
+#endif
+// values (TPA_MV2_SEGSCAN: padded by one double per 8), row pointers, row sums.
+// The size matters: 2 KB more per CTA cost 4% at C2 and 22% at C4 (less L1).
+constexpr size_t kMvValPad = TPA_MV2_SEGSCAN ? kMvTileNnz / 8 : 0;
+// row offsets inside the tile (int32, relative to the tile's first nonzero)
+constexpr size_t kMvRpBytes = ((kMvTileRows + 1) * 4 + 7) / 8 * 8;
+constexpr size_t kMvDynSmem = ((size_t)kMvTileNnz + kMvValPad) * 8 + kMvRpBytes + (size_t)kMvTileRows * 8;
 
 struct MvArgs {
     StepArgs s;
@@ -88,9 +96,9 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     // row pointers, row sums
     extern __shared__ __align__(16) unsigned char s_mv[];
     double* s_vals = reinterpret_cast<double*>(s_mv);
-    int64_t* s_rp = reinterpret_cast<int64_t*>(s_vals + kMvTileNnz);
-    double* s_y = reinterpret_cast<double*>(s_rp + kMvTileRows + 1);
-    __shared__ double s_red[kThreads];
+    int* s_rp = reinterpret_cast<int*>(s_vals + kMvTileNnz + kMvValPad);  // row starts - nb
+    double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + kMvRpBytes);
+    __shared__ double s_red[kThreads / 32];
     __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
             const int k = tid + j * kThreads;
             u[j] = k < nnz ? ld_stream_u32(a.col + nb + k) : 0u;
         }
-        for (uint32_t r = tid; r <= nrows; r += kThreads) s_rp[r] = a.row_ptr[rb + r];
+        for (uint32_t r = tid; r <= nrows; r += kThreads) s_rp[r] = (int)(a.row_ptr[rb + r] - nb);
         uint32_t dg[RPT];
         double ac[RPT];
 #pragma unroll
@@ -159,6 +167,110 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
             const int k = tid + j * kThreads;
             v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
         }
+#if TPA_MV2_SEGSCAN
+        // (A/B experiment, measured slower: C2 0.126-0.139 ms vs 0.110, C4
+        // 3.54-4.25 vs 3.22; 48-62 registers)
+        // nnz-balanced row sums: thread t owns positions [8t, 8t + 8) of the
+        // tile; a segmented scan (in-thread sequential, then a fixed
+        // shuffle / warp tree across threads) carries rows that span
+        // threads.  Every thread does the same work whatever the row lengths,
+        // so no thread idles at the barrier behind a long row.  The order is
+        // a function of the tile (identical in a row partition, which cuts at
+        // tile starts).  s_vals is padded (one double per 8) so the blocked
+        // reads below are bank-conflict free.
+        static_assert(kMvTileNnz == 8 * kThreads, "segmented sums assume 8 nnz per thread");
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int k = tid + j * kThreads;
+            if (k < nnz) s_vals[k + (k >> 3)] = v[j];
+        }
+        for (uint32_t r = tid; r < nrows; r += kThreads) s_y[r] = 0.0;  // empty rows stay 0
+        __syncthreads();
+        {
+            const int p0 = tid * 8;
+            // the row holding position p0: the last r with s_rp[r] <= p0
+            int r = 0;
+            if (p0 < nnz) {
+                int lo = 0, hi = (int)nrows - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_rp[mid] <= p0) lo = mid;
+                    else hi = mid - 1;
+                }
+                r = lo;
+            }
+            const int r_first = r;
+            int next = p0 < nnz ? s_rp[r + 1] : 0;  // end of row r
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = p0 + i < nnz ? s_vals[p0 + i + (p0 >> 3)] : 0.0;
+            // pass 1: the thread's aggregate (sum since its last row start)
+            uint32_t starts = 0;  // bit i: position p0 + i starts a row
+            {
+                int rr = r, nx = next;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = p0 + i;
+                    if (k < nnz && k == nx) {
+                        starts |= 1u << i;
+                        while (s_rp[rr + 1] <= k) ++rr;
+                        nx = s_rp[rr + 1];
+                    }
+                }
+            }
+            if (p0 < nnz && s_rp[r] == p0) starts |= 1u;
+            double agg = 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) agg = ((starts >> i) & 1u) ? x[i] : dadd(agg, x[i]);
+            int aflag = starts != 0;
+            // exclusive segmented scan of (agg, aflag) over the CTA
+            double iv = agg;
+            int ifl = aflag;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double pv = __shfl_up_sync(0xffffffffu, iv, o);
+                const int pf = __shfl_up_sync(0xffffffffu, ifl, o);
+                if (lane >= o && !ifl) iv = dadd(pv, iv);
+                if (lane >= o) ifl |= pf;
+            }
+            __shared__ double s_wv[kThreads / 32];
+            __shared__ int s_wf[kThreads / 32];
+            if (lane == 31) {
+                s_wv[warp] = iv;
+                s_wf[warp] = ifl;
+            }
+            __syncthreads();
+            double cv = 0.0;  // carry from the warps before this one
+            int cf = 0;
+            for (int w = 0; w < warp; ++w) {
+                cv = s_wf[w] ? s_wv[w] : dadd(cv, s_wv[w]);
+                cf |= s_wf[w];
+            }
+            double ev = __shfl_up_sync(0xffffffffu, iv, 1);  // exclusive within the warp
+            int ef = __shfl_up_sync(0xffffffffu, ifl, 1);
+            if (lane == 0) {
+                ev = 0.0;
+                ef = 0;
+            }
+            const double carry = ef ? ev : dadd(cv, ev);
+            (void)cf;
+            // pass 2: running sums; a row's value is final at its last position
+            double run = carry;
+            int rr = r_first, nx = next;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = p0 + i;
+                if (k >= nnz) break;
+                run = ((starts >> i) & 1u) ? x[i] : dadd(run, x[i]);
+                if (k == nx - 1) {
+                    s_y[rr] = run;
+                    // on to the row holding position k + 1 (past empty rows)
+                    while (rr + 1 < (int)nrows && s_rp[rr + 1] <= k + 1) ++rr;
+                    nx = s_rp[rr + 1];
+                }
+            }
+        }
+#else
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int k = tid + j * kThreads;
@@ -167,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         __syncthreads();
         // short rows: one thread, ascending-source sequential sum (reference order)
         for (uint32_t r = tid; r < nrows; r += kThreads) {
-            const int lo = (int)(s_rp[r] - nb), hi = (int)(s_rp[r + 1] - nb);
+            const int lo = s_rp[r], hi = s_rp[r + 1];
             if (hi - lo <= kMvShortRow) {
                 double s = 0.0;
                 for (int k = lo; k < hi; ++k) s = dadd(s, s_vals[k]);
@@ -177,19 +289,20 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         // longer rows of the tile: one warp each, lane-strided + butterfly
         for (uint32_t base = warp * 32; base < nrows; base += kThreads) {
             const uint32_t r = base + lane;
-            const int len = r < nrows ? (int)(s_rp[r + 1] - s_rp[r]) : 0;
+            const int len = r < nrows ? (s_rp[r + 1] - s_rp[r]) : 0;
             unsigned mask = __ballot_sync(0xffffffffu, len > kMvShortRow);
             while (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const uint32_t rr = base + j;
-                const int lo = (int)(s_rp[rr] - nb), hi = (int)(s_rp[rr + 1] - nb);
+                const int lo = s_rp[rr], hi = s_rp[rr + 1];
                 double s = 0.0;
                 for (int k = lo + lane; k < hi; k += 32) s = dadd(s, s_vals[k]);
                 s = warp_sum(s);
                 if (lane == 0) s_y[rr] = s;
             }
         }
+#endif
         __syncthreads();
         // epilogue with the prefetched degree / accumulator of each row
 #pragma unroll

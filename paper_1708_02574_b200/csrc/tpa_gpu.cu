@@ -897,11 +897,11 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             {
                 static const bool smem1 = [] {
                     CK(cudaFuncSetAttribute(k_step_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kMvDynSmem));
+                                            (int)kMv1DynSmem));
                     return true;
                 }();
                 (void)smem1;
-                k_step_spmv<<<grid, block, kMvDynSmem, g->stream>>>(a);
+                k_step_spmv<<<grid, block, kMv1DynSmem, g->stream>>>(a);
             }
             break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;

@@ -1,6 +1,15 @@
 """D2H bandwidth into pinned memory: one copy vs k concurrent copies on k streams."""
+import os
+import sys
 import time
 import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if len(sys.argv) > 1 and sys.argv[1] == "local":
+    import bench
+    c = bench.gpu_local_cpus(0)
+    print("local cpus", sorted(c) if c else None)
+    if c:
+        os.sched_setaffinity(0, c)
 N = 268 << 20
 src = torch.empty(N, dtype=torch.uint8, device="cuda")
 dst = torch.empty(N, dtype=torch.uint8, pin_memory=True)
