@@ -32,7 +32,7 @@ namespace tpa {
 #define TPA_MM5_UNROLL_H 0
 #endif
 #ifndef TPA_MM5_SLIM
-#define TPA_MM5_SLIM 0
+#define TPA_MM5_SLIM 1  // B = 16: 1.018 -> 0.997 ms per C2 batch; B = 32 / 64 within noise
 #endif
 #ifndef TPA_MM5_MINB
 #define TPA_MM5_MINB 8
