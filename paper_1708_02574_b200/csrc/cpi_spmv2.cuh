@@ -36,8 +36,19 @@ struct PeerOut {
 // The size matters: 2 KB more per CTA cost 4% at C2 and 22% at C4 (less L1).
 constexpr size_t kMvValPad = TPA_MV2_SEGSCAN ? kMvTileNnz / 8 : 0;
 // row offsets inside the tile (int32, relative to the tile's first nonzero)
-constexpr size_t kMvRpBytes = ((kMvTileRows + 1) * 4 + 7) / 8 * 8;
-constexpr size_t kMvDynSmem = ((size_t)kMvTileNnz + kMvValPad) * 8 + kMvRpBytes + (size_t)kMvTileRows * 8;
+template <int kRows>
+__host__ __device__ constexpr size_t mv_rp_bytes() { return ((kRows + 1) * 4 + 7) / 8 * 8; }
+template <int kRows>
+__host__ __device__ constexpr size_t mv_dyn_smem() { return ((size_t)kMvTileNnz + kMvValPad) * 8 + mv_rp_bytes<kRows>() + (size_t)kRows * 8; }
+constexpr size_t kMvDynSmem = mv_dyn_smem<kMvTileRows>();
+// Rows per SpMV tile: 512, or 256 once the share vector outgrows half the L2
+// (n x 8 bytes > 64 MB: C4 3.135 -> 3.005 ms, C5 47.9 -> 46.0 ms per sweep; at
+// C2 256-row tiles cost 3%).  A function of the GLOBAL node count, so a row
+// partition tiles its rows exactly as the whole graph does (partition.py).
+inline int mv_tile_rows(uint64_t n_global) {
+    if (const char* e = std::getenv("TPA_MV_TILE_ROWS")) return std::atoi(e) == 256 ? 256 : kMvTileRows;
+    return n_global * 8 > (64ull << 20) ? 256 : kMvTileRows;
+}
 
 struct MvArgs {
     StepArgs s;
@@ -85,10 +96,10 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
 #define TPA_MV2_EARLY_EXIT 1
 #endif
 #ifdef TPA_MV2_MINB  // A/B knob; the default (no minimum) compiles to 40 registers, 6 CTAs/SM
-template <bool kRowFx>
+template <bool kRowFx, int kRows = kMvTileRows>
 __global__ void __launch_bounds__(kThreads, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
 #else
-template <bool kRowFx>
+template <bool kRowFx, int kRows = kMvTileRows>
 __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
 #endif
     const StepArgs& a = M.s;
@@ -97,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     extern __shared__ __align__(16) unsigned char s_mv[];
     double* s_vals = reinterpret_cast<double*>(s_mv);
     int* s_rp = reinterpret_cast<int*>(s_vals + kMvTileNnz + kMvValPad);  // row starts - nb
-    double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + kMvRpBytes);
+    double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + mv_rp_bytes<kRows>());
     __shared__ double s_red[kThreads / 32];
     __shared__ uint32_t s_ticket;
 
@@ -143,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         const uint32_t nrows = re - rb;
         const int nnz = (int)(ne - nb);
         constexpr int U = kMvTileNnz / kThreads;
-        constexpr int RPT = kMvTileRows / kThreads;  // rows per thread
+        constexpr int RPT = kRows / kThreads;  // rows per thread
         // ---- round trip 1: indices, row pointers, degrees, accumulators ----
         uint32_t u[U];
 #pragma unroll

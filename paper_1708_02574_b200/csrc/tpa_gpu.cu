@@ -514,6 +514,7 @@ struct tpa_graph {
     DevBuf row_ptr, col, deg;
     DevBuf out_off, out_tgt;  // the out-edge CSR itself (frontier push-marking)
     Schedule mv;  // SpMV work items
+    int mv_rows = kMvTileRows;  // rows per SpMV tile (mv_tile_rows of the global node count)
     std::unique_ptr<Relabel> rl;  // relabelled twin for dense-start B = 1 runs (tpa_relabel.cuh), built lazily
     LongRows longs;
     uint32_t n_blocks = 0;  // kMmRows-row blocks
@@ -889,6 +890,15 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                     }();
                     (void)smem_rf;
                     k_step_spmv2<true><<<grid, block, kMvDynSmem, g->stream>>>(M);
+                } else if (g->mv_rows == 256) {
+                    static const bool smem256 = [] {
+                        CK(cudaFuncSetAttribute(k_step_spmv2<false, 256>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)mv_dyn_smem<256>()));
+                        return true;
+                    }();
+                    (void)smem256;
+                    k_step_spmv2<false, 256><<<grid, block, mv_dyn_smem<256>(), g->stream>>>(M);
                 } else {
                     k_step_spmv2<false><<<grid, block, kMvDynSmem, g->stream>>>(M);
                 }
@@ -1269,7 +1279,8 @@ static void require_solo_part(const tpa_graph* g) {
 // SpMM long-row segments and short-row blocks.
 static void build_schedules(tpa_graph* g, const std::vector<int64_t>& rp, uint32_t n) {
     cudaStream_t s = g->stream;
-    auto mv = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
+    g->mv_rows = mv_tile_rows(g->part ? g->part->n_global : n);
+    auto mv = build_items(rp, n, kMvTileNnz, (uint32_t)g->mv_rows, kMvTileNnz);
     if (mv.size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
     {
         // SpMM long rows: kLong-nnz segments, longest rows first

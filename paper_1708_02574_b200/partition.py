@@ -14,6 +14,8 @@ Queries (independent seeds) run on whole-graph replicas (``DeviceGraph``).
 """
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from typing import Optional, Sequence
 
@@ -30,10 +32,19 @@ COMM_ID_BYTES = 128
 TILE_NNZ, TILE_ROWS = 2048, 512
 
 
+def tile_rows(n: int) -> int:
+    """Rows per SpMV tile for a graph of n nodes (cpi_spmv2.cuh mv_tile_rows)."""
+    e = os.environ.get("TPA_MV_TILE_ROWS")
+    if e is not None:
+        return 256 if int(e) == 256 else TILE_ROWS
+    return 256 if n * 8 > (64 << 20) else TILE_ROWS
+
+
 def item_starts(rp: np.ndarray, n: int) -> list:
     """Rows where the whole graph's SpMV tiling (tpa_gpu.cu build_items)
     starts an item: greedy tiles of <= TILE_ROWS rows / TILE_NNZ nnz, rows
     longer than TILE_NNZ alone."""
+    rows = tile_rows(n)
     starts, r = [], 0
     while r < n:
         if rp[r + 1] - rp[r] > TILE_NNZ:
@@ -41,7 +52,7 @@ def item_starts(rp: np.ndarray, n: int) -> list:
             r += 1
             continue
         start, nnz = r, 0
-        while r < n and r - start < TILE_ROWS:
+        while r < n and r - start < rows:
             L = rp[r + 1] - rp[r]
             if L > TILE_NNZ or (r > start and nnz + L > TILE_NNZ):
                 break
