@@ -120,10 +120,15 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler is live before the timed region starts (short runs
+            # would otherwise end before its first line)
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:  # noqa: BLE001
             self.proc = None
         return self

@@ -43,4 +43,4 @@ def test_gpu_arm_line():
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert 0 < r["frac"] < 1
-    assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["clocks"]["sm_max_mhz"]
+    assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["clocks"]["samples"] > 0
