@@ -195,11 +195,14 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_per_launch(kernel):
+def traffic_per_launch(kernel, cfg_name=None):
+    """DRAM bytes per launch of `kernel` from one ncu capture (profiles/traffic.json),
+    keyed "<config>:<kernel>" where the config changes the working set."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
+        return t.get(f"{cfg_name}:{kernel}", t.get(kernel) if cfg_name in (None, "c2", "c1") else None)
     except Exception:  # noqa: BLE001
         return None
 
@@ -484,7 +487,7 @@ def run_ours(args):
         pass
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
-                "traffic": traffic_per_launch(kname), "algorithmic_bytes_per_launch": bytes_launch,
+                "traffic": traffic_per_launch(kname, cfg_name), "algorithmic_bytes_per_launch": bytes_launch,
                 "avg_launch_ms": avg_ms, "launches_timed": mm_cnt if batch > 1 else mv_cnt,
                 "share_of_step": share, "per_sweep": per_sweep,
                 "survey_a_step_bytes": a_step(n, m, Bk, 1),

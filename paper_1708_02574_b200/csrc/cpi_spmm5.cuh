@@ -31,6 +31,9 @@ namespace tpa {
 #ifndef TPA_MM5_UNROLL_H
 #define TPA_MM5_UNROLL_H 0
 #endif
+#ifndef TPA_MM5_TIMING_NO_LIVE
+#define TPA_MM5_TIMING_NO_LIVE 0
+#endif
 #ifndef TPA_MM5_SLIM
 #define TPA_MM5_SLIM 1  // B = 16: 1.018 -> 0.997 ms per C2 batch; B = 32 / 64 within noise
 #endif
@@ -224,7 +227,12 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             return e < e1 ? ld_stream_u32(col + e) : 0u;
         };
         auto bits32 = [&](uint32_t u, int64_t base) -> uint32_t {
+#if TPA_MM5_TIMING_NO_LIVE  // TIMING PROBE ONLY (wrong results): no frontier lookups
+            (void)u; (void)base;
+            return 0xffffffffu;
+#else
             return (nz && base + lane < e1) ? __ldg(nz + (u >> 5)) : 0xffffffffu;
+#endif
         };
         if (any_active && e1 > e0) {
             uint32_t i0 = idx32(e0), i1 = idx32(e0 + 32);
