@@ -92,6 +92,10 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
 // tiling only; a row partition cuts at tile starts, tpa_part.cuh).
 // kRowFx = true (the relabelled twin, tpa_relabel.cuh): every row's |y| goes
 // into exact fixed point on its own, so any tiling gives the same totals.
+#ifndef TPA_MV2_FX_SLOTS
+#define TPA_MV2_FX_SLOTS 1
+#endif
+constexpr int kMvFxSlots = TPA_MV2_FX_SLOTS;  // [4 x slots] fixed-point accumulators (w.fx, B = 1)
 #ifndef TPA_MV2_EARLY_EXIT  // 1: 0.1102 -> 0.1097 ms per C2 sweep, 3.232 -> 3.220 at C4
 #define TPA_MV2_EARLY_EXIT 1
 #endif
@@ -114,6 +118,9 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t item = blockIdx.x;
+    // tile totals spread over kMvFxSlots accumulator pairs: fewer same-address
+    // atomics serialising in one L2 slice (the last CTA adds the slots)
+    const int fx_slot = (int)(item % kMvFxSlots);
     const ColState st = a.state_in[0];
     const uint2 it = a.items[item];
     const uint32_t rb = it.x, re = it.y & ~kLongFlag;
@@ -375,12 +382,12 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
             unsigned long long h = 0, l = 0;
             if (tl1 != 0.0) {
                 fx_add(h, l, tl1);
-                fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
+                fx_atomic_add(&M.fx[4 * fx_slot + 0], &M.fx[4 * fx_slot + 1], h, l);
             }
             if (tdm != 0.0) {
                 h = l = 0;
                 fx_add(h, l, tdm);
-                fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
+                fx_atomic_add(&M.fx[4 * fx_slot + 2], &M.fx[4 * fx_slot + 3], h, l);
             }
         }
     }
@@ -400,8 +407,16 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     if (s_ticket != gridDim.x - 1 || tid != 0) return;
 #endif
     __threadfence();
-    const unsigned long long h0 = atomicAdd(&M.fx[0], 0ull), l0 = atomicAdd(&M.fx[1], 0ull);
-    const unsigned long long h1 = atomicAdd(&M.fx[2], 0ull), l1 = atomicAdd(&M.fx[3], 0ull);
+    // exact 128-bit sums of the slots (order-free)
+    unsigned long long h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int k = 0; k < kMvFxSlots; ++k) {
+        const unsigned long long a0 = atomicAdd(&M.fx[4 * k + 0], 0ull), b0 = atomicAdd(&M.fx[4 * k + 1], 0ull);
+        const unsigned long long a1 = atomicAdd(&M.fx[4 * k + 2], 0ull), b1 = atomicAdd(&M.fx[4 * k + 3], 0ull);
+        l0 += b0;
+        h0 += a0 + (l0 < b0 ? 1ull : 0ull);
+        l1 += b1;
+        h1 += a1 + (l1 < b1 ? 1ull : 0ull);
+    }
     if (M.limbs) {
         // a partition's totals: all-reduced, then k_part_finalize advances the state
         fx_to_limbs(h0, l0, M.limbs);
@@ -415,7 +430,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         // last CTA: cpi.cpp:73-80
         a.state_out[0] = advance_state(st, fx_decode(h0, l0), fx_decode(h1, l1), a);
     }
-    M.fx[0] = M.fx[1] = M.fx[2] = M.fx[3] = 0ull;
+    for (int k = 0; k < 4 * kMvFxSlots; ++k) M.fx[k] = 0ull;
     *a.done_cnt = 0;
 }
 

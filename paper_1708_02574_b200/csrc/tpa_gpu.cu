@@ -600,7 +600,7 @@ struct tpa_graph {
         }
         w.state.ensure(2 * (size_t)B * sizeof(ColState), stream);
         if (B == 1 && !w.fx.p) {
-            w.fx.ensure(4 * 8, stream);
+            w.fx.ensure(4 * 8 * kMvFxSlots, stream);
             CK(cudaMemsetAsync(w.fx.p, 0, w.fx.bytes, stream));
             w.long_cnt.ensure((size_t)std::max<uint32_t>(longs.n_long, 1) * 4, stream);
             w.seg_part.ensure((size_t)std::max<uint32_t>(longs.n_segs, 1) * 8, stream);
