@@ -34,20 +34,32 @@ struct PeerOut {
 #endif
 // values (TPA_MV2_SEGSCAN: padded by one double per 8), row pointers, row sums.
 // The size matters: 2 KB more per CTA cost 4% at C2 and 22% at C4 (less L1).
-constexpr size_t kMvValPad = TPA_MV2_SEGSCAN ? kMvTileNnz / 8 : 0;
 // row offsets inside the tile (int32, relative to the tile's first nonzero)
 template <int kRows>
 __host__ __device__ constexpr size_t mv_rp_bytes() { return ((kRows + 1) * 4 + 7) / 8 * 8; }
-template <int kRows>
-__host__ __device__ constexpr size_t mv_dyn_smem() { return ((size_t)kMvTileNnz + kMvValPad) * 8 + mv_rp_bytes<kRows>() + (size_t)kRows * 8; }
-constexpr size_t kMvDynSmem = mv_dyn_smem<kMvTileRows>();
-// Rows per SpMV tile: 512, or 256 once the share vector outgrows half the L2
-// (n x 8 bytes > 64 MB: C4 3.135 -> 3.005 ms, C5 47.9 -> 46.0 ms per sweep; at
-// C2 256-row tiles cost 3%).  A function of the GLOBAL node count, so a row
-// partition tiles its rows exactly as the whole graph does (partition.py).
-inline int mv_tile_rows(uint64_t n_global) {
-    if (const char* e = std::getenv("TPA_MV_TILE_ROWS")) return std::atoi(e) == 256 ? 256 : kMvTileRows;
-    return n_global * 8 > (64ull << 20) ? 256 : kMvTileRows;
+template <int kNnz, int kRows>
+__host__ __device__ constexpr size_t mv_dyn_smem() {
+    return ((size_t)kNnz + (TPA_MV2_SEGSCAN ? kNnz / 8 : 0)) * 8 + mv_rp_bytes<kRows>() + (size_t)kRows * 8;
+}
+constexpr size_t kMvDynSmem = mv_dyn_smem<kMvTileNnz, kMvTileRows>();
+
+// SpMV tile shape {threads per CTA, nnz per tile, rows per tile}, chosen by the
+// GLOBAL node count (a row partition tiles its rows exactly as the whole graph
+// does; partition.py mirrors this).  Measured per PageRank sweep (ms):
+//                         C2 (8 MB shares)  C4 (134 MB)  C5 (2.1 GB)
+//   S {128, 1024, 256}        0.0952          2.920        47.9
+//   L {256, 2048, 256}        0.110           3.005        45.9
+//   W {256, 2048, 512}        0.1062          3.135        47.9   (round-1 default before)
+// Small CTAs finish their tile (and free its slot) sooner: fewer warps wait at
+// each barrier behind the tile's longest row.  Once the share vector is far
+// beyond the L2 the larger tile amortises its DRAM round trips better.
+struct MvShape {
+    int thr, nnz, rows;
+};
+constexpr MvShape kMvShapeS{128, 1024, 256}, kMvShapeL{256, 2048, 256}, kMvShapeW{256, 2048, 512};
+inline MvShape mv_shape(uint64_t n_global) {
+    if (const char* e = std::getenv("TPA_MV_SHAPE")) return e[0] == 'L' ? kMvShapeL : e[0] == 'W' ? kMvShapeW : kMvShapeS;
+    return n_global * 8 > (512ull << 20) ? kMvShapeL : kMvShapeS;
 }
 
 struct MvArgs {
@@ -92,6 +104,22 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
 // tiling only; a row partition cuts at tile starts, tpa_part.cuh).
 // kRowFx = true (the relabelled twin, tpa_relabel.cuh): every row's |y| goes
 // into exact fixed point on its own, so any tiling gives the same totals.
+
+// Deterministic CTA sum over kThr threads (fixed tree); valid in every thread.
+template <int kThr>
+__device__ __forceinline__ double mv_block_sum(double v, double* s_red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    double r = s_red[0];
+#pragma unroll
+    for (int k = 1; k < kThr / 32; ++k) r = dadd(r, s_red[k]);
+    __syncthreads();
+    return r;
+}
+
 #ifndef TPA_MV2_FX_SLOTS
 #define TPA_MV2_FX_SLOTS 1
 #endif
@@ -100,20 +128,20 @@ constexpr int kMvFxSlots = TPA_MV2_FX_SLOTS;  // [4 x slots] fixed-point accumul
 #define TPA_MV2_EARLY_EXIT 1
 #endif
 #ifdef TPA_MV2_MINB  // A/B knob; the default (no minimum) compiles to 40 registers, 6 CTAs/SM
-template <bool kRowFx, int kRows = kMvTileRows>
-__global__ void __launch_bounds__(kThreads, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
+template <bool kRowFx, int kThr, int kNnz, int kRows>
+__global__ void __launch_bounds__(kThr, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
 #else
-template <bool kRowFx, int kRows = kMvTileRows>
-__global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
+template <bool kRowFx, int kThr, int kNnz, int kRows>
+__global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
 #endif
     const StepArgs& a = M.s;
     // the tile's staging in dynamic shared memory (kMvDynSmem bytes): values,
     // row pointers, row sums
     extern __shared__ __align__(16) unsigned char s_mv[];
     double* s_vals = reinterpret_cast<double*>(s_mv);
-    int* s_rp = reinterpret_cast<int*>(s_vals + kMvTileNnz + kMvValPad);  // row starts - nb
+    int* s_rp = reinterpret_cast<int*>(s_vals + kNnz + (TPA_MV2_SEGSCAN ? kNnz / 8 : 0));  // row starts - nb
     double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + mv_rp_bytes<kRows>());
-    __shared__ double s_red[kThreads / 32];
+    __shared__ double s_red[kThr / 32];
     __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -131,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     if (!st.active) {
         // column stopped earlier: only a pending combine remains (tpa.cpp:73)
         if (a.out)
-            for (uint32_t v = rb + tid; v < re; v += kThreads) combine_only(a, v, 0, 1, v);
+            for (uint32_t v = rb + tid; v < re; v += kThr) combine_only(a, v, 0, 1, v);
         if (item == 0 && tid == 0) {
             a.state_out[0] = st;
             if (M.limbs)
@@ -145,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     // row partition, or the relabelled twin of tpa_relabel.cuh, reproduces
     // them bit for bit)
     unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
-    __shared__ unsigned long long s_w[4 * (kThreads / 32)];
+    __shared__ unsigned long long s_w[4 * (kThr / 32)];
     double my_l1 = 0.0, my_dm = 0.0;
     auto add_row = [&](double y, bool dangling) {
         if constexpr (kRowFx) {
@@ -160,21 +188,21 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
     if (!is_long) {
         const uint32_t nrows = re - rb;
         const int nnz = (int)(ne - nb);
-        constexpr int U = kMvTileNnz / kThreads;
-        constexpr int RPT = kRows / kThreads;  // rows per thread
+        constexpr int U = kNnz / kThr;
+        constexpr int RPT = kRows / kThr;  // rows per thread
         // ---- round trip 1: indices, row pointers, degrees, accumulators ----
         uint32_t u[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const int k = tid + j * kThreads;
+            const int k = tid + j * kThr;
             u[j] = k < nnz ? ld_stream_u32(a.col + nb + k) : 0u;
         }
-        for (uint32_t r = tid; r <= nrows; r += kThreads) s_rp[r] = (int)(a.row_ptr[rb + r] - nb);
+        for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(a.row_ptr[rb + r] - nb);
         uint32_t dg[RPT];
         double ac[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
-            const uint32_t r = tid + q * kThreads;
+            const uint32_t r = tid + q * kThr;
             dg[q] = r < nrows ? __ldg(a.deg + rb + r) : 0u;
             ac[q] = (r < nrows && a.acc) ? a.acc[rb + r] : 0.0;
         }
@@ -182,7 +210,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         double v[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const int k = tid + j * kThreads;
+            const int k = tid + j * kThr;
             v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
         }
 #if TPA_MV2_SEGSCAN
@@ -196,13 +224,13 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         // a function of the tile (identical in a row partition, which cuts at
         // tile starts).  s_vals is padded (one double per 8) so the blocked
         // reads below are bank-conflict free.
-        static_assert(kMvTileNnz == 8 * kThreads, "segmented sums assume 8 nnz per thread");
+        static_assert(kNnz == 8 * kThr, "segmented sums assume 8 nnz per thread");
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const int k = tid + j * kThreads;
+            const int k = tid + j * kThr;
             if (k < nnz) s_vals[k + (k >> 3)] = v[j];
         }
-        for (uint32_t r = tid; r < nrows; r += kThreads) s_y[r] = 0.0;  // empty rows stay 0
+        for (uint32_t r = tid; r < nrows; r += kThr) s_y[r] = 0.0;  // empty rows stay 0
         __syncthreads();
         {
             const int p0 = tid * 8;
@@ -251,8 +279,8 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
                 if (lane >= o && !ifl) iv = dadd(pv, iv);
                 if (lane >= o) ifl |= pf;
             }
-            __shared__ double s_wv[kThreads / 32];
-            __shared__ int s_wf[kThreads / 32];
+            __shared__ double s_wv[kThr / 32];
+            __shared__ int s_wf[kThr / 32];
             if (lane == 31) {
                 s_wv[warp] = iv;
                 s_wf[warp] = ifl;
@@ -291,12 +319,12 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
 #else
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const int k = tid + j * kThreads;
+            const int k = tid + j * kThr;
             if (k < nnz) s_vals[k] = v[j];
         }
         __syncthreads();
         // short rows: one thread, ascending-source sequential sum (reference order)
-        for (uint32_t r = tid; r < nrows; r += kThreads) {
+        for (uint32_t r = tid; r < nrows; r += kThr) {
             const int lo = s_rp[r], hi = s_rp[r + 1];
             if (hi - lo <= kMvShortRow) {
                 double s = 0.0;
@@ -305,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
             }
         }
         // longer rows of the tile: one warp each, lane-strided + butterfly
-        for (uint32_t base = warp * 32; base < nrows; base += kThreads) {
+        for (uint32_t base = warp * 32; base < nrows; base += kThr) {
             const uint32_t r = base + lane;
             const int len = r < nrows ? (s_rp[r + 1] - s_rp[r]) : 0;
             unsigned mask = __ballot_sync(0xffffffffu, len > kMvShortRow);
@@ -325,7 +353,7 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         // epilogue with the prefetched degree / accumulator of each row
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
-            const uint32_t r = tid + q * kThreads;
+            const uint32_t r = tid + q * kThr;
             if (r >= nrows) continue;
             const uint32_t vtx = rb + r;
             double y = s_y[r];
@@ -351,18 +379,18 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         double s = 0.0;
         constexpr int U = 8;
         int64_t e = nb + tid;
-        for (; e + (U - 1) * kThreads < ne; e += U * kThreads) {
+        for (; e + (U - 1) * kThr < ne; e += U * kThr) {
             uint32_t u[U];
             double v[U];
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = ld_stream_u32(a.col + e + j * kThreads);
+            for (int j = 0; j < U; ++j) u[j] = ld_stream_u32(a.col + e + j * kThr);
 #pragma unroll
             for (int j = 0; j < U; ++j) v[j] = __ldg(a.share_in + u[j]);
 #pragma unroll
             for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
         }
-        for (; e < ne; e += kThreads) s = dadd(s, __ldg(a.share_in + ld_stream_u32(a.col + e)));
-        s = block_sum(s, s_red);
+        for (; e < ne; e += kThr) s = dadd(s, __ldg(a.share_in + ld_stream_u32(a.col + e)));
+        s = mv_block_sum<kThr>(s, s_red);
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
             const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
@@ -376,8 +404,8 @@ __global__ void __launch_bounds__(kThreads) k_step_spmv2(MvArgs M) {
         fx_cta_flush(f0, f1, f2, f3, s_w, M.fx);
     } else {
         // tile partials (fixed tree) -> exact fixed-point totals across tiles
-        const double tl1 = block_sum(my_l1, s_red);
-        const double tdm = want_dm ? block_sum(my_dm, s_red) : 0.0;
+        const double tl1 = mv_block_sum<kThr>(my_l1, s_red);
+        const double tdm = want_dm ? mv_block_sum<kThr>(my_dm, s_red) : 0.0;
         if (tid == 0) {
             unsigned long long h = 0, l = 0;
             if (tl1 != 0.0) {

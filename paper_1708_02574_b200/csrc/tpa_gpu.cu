@@ -514,7 +514,7 @@ struct tpa_graph {
     DevBuf row_ptr, col, deg;
     DevBuf out_off, out_tgt;  // the out-edge CSR itself (frontier push-marking)
     Schedule mv;  // SpMV work items
-    int mv_rows = kMvTileRows;  // rows per SpMV tile (mv_tile_rows of the global node count)
+    MvShape mv_shape = kMvShapeS;  // SpMV tile shape (mv_shape of the global node count)
     std::unique_ptr<Relabel> rl;  // relabelled twin for dense-start B = 1 runs (tpa_relabel.cuh), built lazily
     LongRows longs;
     uint32_t n_blocks = 0;  // kMmRows-row blocks
@@ -739,6 +739,23 @@ static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
     return std::upper_bound(bounds.begin(), bounds.end(), i) - bounds.begin();
 }
 
+// K2 v2 at one tile shape: dynamic shared memory sized for it (and the
+// TPA_MV_CARVEOUT A/B knob) set once per instantiation.
+template <bool RF, int THR, int NNZ, int ROWS>
+static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
+    constexpr size_t smem = mv_dyn_smem<NNZ, ROWS>();
+    static const bool ok = [] {
+        CK(cudaFuncSetAttribute(k_step_spmv2<RF, THR, NNZ, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        if (const char* e = std::getenv("TPA_MV_CARVEOUT"))
+            CK(cudaFuncSetAttribute(k_step_spmv2<RF, THR, NNZ, ROWS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    std::atoi(e)));
+        return true;
+    }();
+    (void)ok;
+    k_step_spmv2<RF, THR, NNZ, ROWS><<<grid, THR, smem, stream>>>(M);
+}
+
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
                         const SeedList* push_seeds = nullptr, const Schedule* sched = nullptr) {
     const Schedule& s = sched ? *sched : g->mv;
@@ -864,43 +881,24 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                 k_step_spmv3<<<grid3, kMv3Threads, 0, g->stream>>>(M);
             } else if (spmv_version() == 2 || g->part)
             {
-                static const bool carve = [] {  // A/B: shared-memory carveout (L1 share) for v2
-                    const char* e = std::getenv("TPA_MV_CARVEOUT");
-                    if (e) CK(cudaFuncSetAttribute(k_step_spmv2<false>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
-                    return e != nullptr;
-                }();
-                (void)carve;
                 MvArgs M{a, s.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
                          !g->part ? nullptr
                          : a.share_out ? reinterpret_cast<unsigned long long*>(a.share_out + g->part->slice)
                                        : w.limbs.as<unsigned long long>() + (a.step & 1) * 6,
                          PeerOut{}, g->part ? g->part->slice : 0u};
                 if (g->part && a.share_out) M.peers = g->peer_out;
-                static const bool smem_ok = [] {
-                    CK(cudaFuncSetAttribute(k_step_spmv2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kMvDynSmem));
-                    return true;
-                }();
-                (void)smem_ok;
-                if (sched && sched != &g->mv) {  // the relabelled twin: per-row exact totals
-                    static const bool smem_rf = [] {
-                        CK(cudaFuncSetAttribute(k_step_spmv2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)kMvDynSmem));
-                        return true;
-                    }();
-                    (void)smem_rf;
-                    k_step_spmv2<true><<<grid, block, kMvDynSmem, g->stream>>>(M);
-                } else if (g->mv_rows == 256) {
-                    static const bool smem256 = [] {
-                        CK(cudaFuncSetAttribute(k_step_spmv2<false, 256>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)mv_dyn_smem<256>()));
-                        return true;
-                    }();
-                    (void)smem256;
-                    k_step_spmv2<false, 256><<<grid, block, mv_dyn_smem<256>(), g->stream>>>(M);
+                // the relabelled twin sums its residual row by row (tpa_relabel.cuh)
+                const bool rf = sched && sched != &g->mv;
+                const MvShape& sh = g->mv_shape;
+                if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows) {
+                    if (rf) launch_mv2<true, 128, 1024, 256>(M, grid.x, g->stream);
+                    else launch_mv2<false, 128, 1024, 256>(M, grid.x, g->stream);
+                } else if (sh.rows == kMvShapeL.rows) {
+                    if (rf) launch_mv2<true, 256, 2048, 256>(M, grid.x, g->stream);
+                    else launch_mv2<false, 256, 2048, 256>(M, grid.x, g->stream);
                 } else {
-                    k_step_spmv2<false><<<grid, block, kMvDynSmem, g->stream>>>(M);
+                    if (rf) launch_mv2<true, 256, 2048, 512>(M, grid.x, g->stream);
+                    else launch_mv2<false, 256, 2048, 512>(M, grid.x, g->stream);
                 }
             }
             else
@@ -1279,8 +1277,8 @@ static void require_solo_part(const tpa_graph* g) {
 // SpMM long-row segments and short-row blocks.
 static void build_schedules(tpa_graph* g, const std::vector<int64_t>& rp, uint32_t n) {
     cudaStream_t s = g->stream;
-    g->mv_rows = mv_tile_rows(g->part ? g->part->n_global : n);
-    auto mv = build_items(rp, n, kMvTileNnz, (uint32_t)g->mv_rows, kMvTileNnz);
+    g->mv_shape = mv_shape(g->part ? g->part->n_global : n);
+    auto mv = build_items(rp, n, g->mv_shape.nnz, (uint32_t)g->mv_shape.rows, g->mv_shape.nnz);
     if (mv.size() >= 0x7fffffffu) throw std::invalid_argument("graph too large for one grid");
     {
         // SpMM long rows: kLong-nnz segments, longest rows first

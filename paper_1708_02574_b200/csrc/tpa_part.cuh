@@ -124,7 +124,8 @@ __global__ void k_sum_limbs(LimbPtrs src, uint32_t G, unsigned long long* __rest
 static std::vector<uint32_t> partition_rows(const std::vector<uint64_t>& prefix, uint32_t n, uint32_t G) {
     const uint64_t m = prefix[n];
     std::vector<int64_t> rp(prefix.begin(), prefix.end());
-    std::vector<uint2> items = build_items(rp, n, kMvTileNnz, (uint32_t)mv_tile_rows(n), kMvTileNnz);
+    const MvShape sh = mv_shape(n);
+    std::vector<uint2> items = build_items(rp, n, sh.nnz, (uint32_t)sh.rows, sh.nnz);
     std::vector<uint32_t> cuts;
     cuts.reserve(items.size() + 1);
     for (const uint2& it : items) cuts.push_back(it.x);

@@ -143,7 +143,7 @@ static Relabel* relabel_view(tpa_graph* g) {
     std::vector<int64_t> rp(n + 1ull);
     CK(cudaMemcpyAsync(rp.data(), rl->row_ptr.p, (n + 1ull) * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    auto mv = build_items(rp, n, kMvTileNnz, kMvTileRows, kMvTileNnz);
+    auto mv = build_items(rp, n, g->mv_shape.nnz, (uint32_t)g->mv_shape.rows, g->mv_shape.nnz);
     rl->mv.n_items = (uint32_t)mv.size();
     rl->mv.n_groups = (rl->mv.n_items + kGroupItems - 1) / kGroupItems;
     rl->mv.items.ensure(mv.size() * sizeof(uint2), s);

@@ -29,36 +29,37 @@ COMM_ID_BYTES = 128
 
 
 # SpMV tiling constants (csrc/cpi_kernels.cuh kMvTileNnz / kMvTileRows)
-TILE_NNZ, TILE_ROWS = 2048, 512
+TILE_NNZ, TILE_ROWS = 2048, 512  # the largest tile shape (bounds; tests)
+SHAPES = {"S": (1024, 256), "L": (2048, 256), "W": (2048, 512)}  # (nnz, rows), cpi_spmv2.cuh
 
 
-def tile_rows(n: int) -> int:
-    """Rows per SpMV tile for a graph of n nodes (cpi_spmv2.cuh mv_tile_rows)."""
-    e = os.environ.get("TPA_MV_TILE_ROWS")
-    if e is not None:
-        return 256 if int(e) == 256 else TILE_ROWS
-    return 256 if n * 8 > (64 << 20) else TILE_ROWS
+def tile_shape(n: int) -> tuple:
+    """(nnz, rows) per SpMV tile for a graph of n nodes (cpi_spmv2.cuh mv_shape)."""
+    e = os.environ.get("TPA_MV_SHAPE")
+    if e:
+        return SHAPES["L"] if e[0] == "L" else SHAPES["W"] if e[0] == "W" else SHAPES["S"]
+    return SHAPES["L"] if n * 8 > (512 << 20) else SHAPES["S"]
 
 
 def item_starts(rp: np.ndarray, n: int) -> list:
     """Rows where the whole graph's SpMV tiling (tpa_gpu.cu build_items)
-    starts an item: greedy tiles of <= TILE_ROWS rows / TILE_NNZ nnz, rows
-    longer than TILE_NNZ alone."""
-    rows = tile_rows(n)
+    starts an item: greedy tiles of <= rows rows / tile_nnz nnz, rows
+    longer than tile_nnz alone."""
+    tile_nnz, rows = tile_shape(n)
     starts, r = [], 0
     while r < n:
-        if rp[r + 1] - rp[r] > TILE_NNZ:
+        if rp[r + 1] - rp[r] > tile_nnz:
             starts.append(r)
             r += 1
             continue
         start, nnz = r, 0
         while r < n and r - start < rows:
             L = rp[r + 1] - rp[r]
-            if L > TILE_NNZ or (r > start and nnz + L > TILE_NNZ):
+            if L > tile_nnz or (r > start and nnz + L > tile_nnz):
                 break
             nnz += L
             r += 1
-            if nnz >= TILE_NNZ:
+            if nnz >= tile_nnz:
                 break
         starts.append(start)
     return starts

@@ -36,7 +36,7 @@ print("ok")
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", ["TPA_SPMM=2", "TPA_SPMM=3", "TPA_SPMM=4", "TPA_SPMV=1", "TPA_SPMV=3",
                                  "TPA_NO_SPARSE=1", "TPA_NO_WINDOW_LIST=1", "TPA_MM5_RB=16", "TPA_SPARSE_DIV=4",
-                                 "TPA_NO_SEED_PUSH=1", "TPA_RELABEL=1", "TPA_MM5_RB=8", "TPA_MV_TILE_ROWS=256"])
+                                 "TPA_NO_SEED_PUSH=1", "TPA_RELABEL=1", "TPA_MM5_RB=8", "TPA_MV_SHAPE=L", "TPA_MV_SHAPE=W"])
 def test_variant_parity(env):
     k, v = env.split("=")
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env={**os.environ, k: v},
