@@ -891,8 +891,8 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                 const bool rf = sched && sched != &g->mv;
                 const MvShape& sh = g->mv_shape;
                 if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows) {
-                    if (rf) launch_mv2<true, 128, 1024, 256>(M, grid.x, g->stream);
-                    else launch_mv2<false, 128, 1024, 256>(M, grid.x, g->stream);
+                    if (rf) launch_mv2<true, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
+                    else launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
                 } else if (sh.rows == kMvShapeL.rows) {
                     if (rf) launch_mv2<true, 256, 2048, 256>(M, grid.x, g->stream);
                     else launch_mv2<false, 256, 2048, 256>(M, grid.x, g->stream);
