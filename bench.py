@@ -18,9 +18,15 @@ roofline fraction of the dominant sweep kernel reported beside it.
 (oracle/_ref/librwrank_ref.so, built from /root/reference/proj/src; the C
 oracle port if that is absent) on the host cores, same config and metric.
 
-Multi-GPU (torchrun, one rank per GPU): seed-parallel replicas -- every rank
-holds the graph, preprocesses, and answers its own full query set (weak
-scaling, no data-path collective).
+Multi-GPU (torchrun, one rank per GPU): the one job strong-scaled --
+PageRank preprocessing row-partitioned across the ranks (one NCCL all-gather of
+the iterate's shares + exact residual limbs per sweep) and the job's queries
+split over the ranks' whole-graph replicas (no data-path collective);
+TPA_BENCH_REPLICAS=1 runs N independent jobs instead (weak scaling).
+
+Configs (--config): c1..c5 of BASELINE.json; c4/c5 graphs are generated and
+built on the GPU (same graph as the host generator); c5 keeps each batch's
+scores in HBM plus the device top-10 (a resident [16][n] output would not fit).
 """
 from __future__ import annotations
 
