@@ -893,9 +893,9 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                 if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows) {
                     if (rf) launch_mv2<true, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
                     else launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
-                } else if (sh.rows == kMvShapeL.rows) {
-                    if (rf) launch_mv2<true, 256, 2048, 256>(M, grid.x, g->stream);
-                    else launch_mv2<false, 256, 2048, 256>(M, grid.x, g->stream);
+                } else if (sh.thr == kMvShapeL.thr && sh.nnz == kMvShapeL.nnz && sh.rows == kMvShapeL.rows) {
+                    if (rf) launch_mv2<true, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
+                    else launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
                 } else {
                     if (rf) launch_mv2<true, 256, 2048, 512>(M, grid.x, g->stream);
                     else launch_mv2<false, 256, 2048, 512>(M, grid.x, g->stream);
