@@ -131,6 +131,9 @@ __device__ __forceinline__ double mv_block_sum(double v, double* s_red) {
     return r;
 }
 
+#ifndef TPA_MV2_PDL  // A/B: programmatic dependent launch between consecutive sweeps
+#define TPA_MV2_PDL 1  // C1 65.4 -> 68.3 GTEPS (launch-bound sweeps), C2 unchanged
+#endif
 #ifndef TPA_MV2_FX_SLOTS
 #define TPA_MV2_FX_SLOTS 1
 #endif
@@ -160,12 +163,20 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     // tile totals spread over kMvFxSlots accumulator pairs: fewer same-address
     // atomics serialising in one L2 slice (the last CTA adds the slots)
     const int fx_slot = (int)(item % kMvFxSlots);
-    const ColState st = a.state_in[0];
-    const uint2 it = a.items[item];
+#if TPA_MV2_PDL
+    // programmatic dependent launch: the next sweep's CTAs may start once
+    // every CTA of this one has; they wait below for this grid to finish
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    const uint2 it = a.items[item];  // the tiling is static: read before the wait
     const uint32_t rb = it.x, re = it.y & ~kLongFlag;
     const bool is_long = (it.y & kLongFlag) != 0;
     const longlong2 nr = M.item_nnz[item];
     const int64_t nb = nr.x, ne = nr.y;
+#if TPA_MV2_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous sweep's shares, acc, state
+#endif
+    const ColState st = a.state_in[0];
 
     if (!st.active) {
         // column stopped earlier: only a pending combine remains (tpa.cpp:73)

@@ -753,7 +753,21 @@ static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
         return true;
     }();
     (void)ok;
+#if TPA_MV2_PDL
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_step_spmv2<RF, THR, NNZ, ROWS>, M));
+#else
     k_step_spmv2<RF, THR, NNZ, ROWS><<<grid, THR, smem, stream>>>(M);
+#endif
 }
 
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
