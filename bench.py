@@ -54,7 +54,10 @@ CONFIGS = {
     "c4": ("rmat", dict(scale=24, edge_factor=32), 1024, 32, 1),
     "c5": ("rmat", dict(scale=28, edge_factor=16), 256, 16, 1),
 }
-DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1]: the metric's single-GPU workload
+# BASELINE.json's metric names no config, so the headline is the largest config
+# that runs on one GPU as BASELINE states it: C4 (R-MAT 24, 529 M edges; C5 is
+# stated as row-sharded across 2/4/8 GPUs)
+DEFAULT_CONFIG = "c4"
 THROTTLE_BITS = {
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
     0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -83,7 +86,7 @@ def build_graph(cfg_name):
     return P.generate_random_graph(p["n"], p["m"], CONFIGS[cfg_name][4])
 
 
-def workload_desc(cfg_name, g, nq, batch):
+def workload_desc(cfg_name, n, m, n_dangling, fingerprint, nq, batch):
     kind, p, *_ = CONFIGS[cfg_name]
     gdesc = (f"R-MAT scale {p['scale']} ef {p['edge_factor']} (a,b,c)=(.57,.19,.19), mt19937_64 seed "
              f"{CONFIGS[cfg_name][4]}, no noise/permutation" if kind == "rmat"
@@ -91,7 +94,7 @@ def workload_desc(cfg_name, g, nq, batch):
     return {
         "workload": f"{cfg_name.upper()}: TPA preprocess (PageRank CPI, window [T,inf)) + {nq} online queries "
                     f"in SpMM batches of {batch}",
-        "graph": gdesc, "n": g.node_count(), "m": g.edge_count(), "dangling": int(len(g.dangling_nodes())),
+        "graph": gdesc, "n": int(n), "m": int(m), "dangling": int(n_dangling), "fingerprint": f"{fingerprint:#018x}",
         "policy": "selfloop", "c": C, "eps": EPS, "S": S, "T": T, "queries": nq, "batch": batch,
         "seeds": "sample_seeds(mt19937_64 seed 1): uniform over non-dangling nodes (rwrank_main.cpp:65-83)",
         "l2": "flushed between timed steps (512 MiB write, untimed)",
@@ -214,89 +217,140 @@ def traffic_per_launch(kernel, cfg_name=None):
 
 
 # ---------------------------------------------------------------------------
-# CPU arm (reference library, or the oracle port)
+# CPU arm (the reference library built from its sources, oracle/_ref)
 # ---------------------------------------------------------------------------
-def cpu_measure(g, seeds, cfg_name, budget_s=20.0, workers=None):
-    """Times the reference CPU path on a bounded sample of the job and
-    extrapolates the job time.  Returns a dict (cpu_baseline)."""
-    from oracle import Oracle, Reference
-    n, m = g.node_count(), g.edge_count()
-    nq = len(seeds)
-    workers = workers or os.cpu_count() or 1
-    if Reference.available():
-        ref = Reference()
-        off = g.out_offsets().astype(np.int64)
-        src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(off))
-        rg = ref.graph_from_edges(n, src, g.out_targets(), "selfloop")
-        assert rg.fingerprint == g.fingerprint()
-        kind = "reference"
-        # preprocess: one full reference call (threads=1: the reference default;
-        # its threaded sweep is slower at these sizes, SURVEY §3(d)); time-box
-        # large graphs to a few dense sweeps and extrapolate x sweeps.
-        t_sweep = rg.time_sweeps(1, C, 1)
-        if t_sweep * 117 <= budget_s * 0.6:
-            stranger, t_pre = rg.time_preprocess(C, EPS, T, 1, keep=True)
-            pre_note = "preprocess timed whole"
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def pagerank_sweeps(c=C, eps=EPS):
+    """Sweeps of the reference PageRank under SelfLoop (mass-preserving):
+    the first i with c(1-c)^i < eps (cpi.cpp:70-81; 116 at c=0.15, eps=1e-9)."""
+    i, r = 0, c
+    while not r < eps:
+        i += 1
+        r = c * (1 - c) ** i
+    return i
+
+
+def reference_graph(cfg_name):
+    """The config's graph built by the reference's own Graph constructor from the
+    benchmark generator's edges (oracle/ref_capi.cpp) -- no product code."""
+    from oracle import Reference
+    if not Reference.available():
+        raise RuntimeError("oracle/_ref/librwrank_ref.so missing: run __graft_entry__.build() with "
+                           "/root/reference present")
+    ref = Reference()
+    kind, p, _, _, seed = CONFIGS[cfg_name]
+    if kind == "rmat":
+        return ref.graph_rmat(p["scale"], p["edge_factor"], 0.57, 0.19, 0.19, seed=seed, threads=0)
+    return ref.graph_random(p["n"], p["m"], seed)
+
+
+class RefCpuSampler:
+    """Times the reference CPU path (tpa.cpp preprocess / query through
+    oracle/_ref, the CLI's timed calls rwrank_main.cpp:122-124, :153-156) on a
+    bounded sample of one job and extrapolates the job time:
+
+    * preprocess: the whole preprocess() when it fits the budget, else
+      116 x one dense propagation_sweep (graph.cpp:230-270) -- at the faster of
+      threads = 1 and threads = min(cores, 64) (picked once, untimed);
+    * queries: a window of the job's seeds (>= 16, >= one per core) run as
+      concurrent single-thread reference query() calls on every core
+      (tpa_test.cpp:148-161: concurrent queries are the reference's contract),
+      a different window each step."""
+
+    def __init__(self, rg, seeds, budget_s=20.0, workers=None):
+        self.rg, self.seeds = rg, np.ascontiguousarray(seeds, np.uint32)
+        self.workers = workers or len(os.sched_getaffinity(0)) or 1
+        self.n, self.m, self.nq = rg.n, rg.m, len(seeds)
+        self.sweeps = pagerank_sweeps()
+        t1 = rg.time_sweeps(1, C, 1)
+        tmax = min(self.workers, 64)
+        tt = rg.time_sweeps(1, C, tmax) if tmax > 1 else t1
+        self.pre_threads = tmax if tt < t1 else 1
+        self.t_sweep_cal = {"threads=1": t1, f"threads={tmax}": tt}
+        t_sw = min(t1, tt)
+        self.whole_pre = t_sw * (self.sweeps + 1) <= budget_s * 0.5
+        self.stranger = np.zeros(self.n)
+        if self.whole_pre:
+            self.stranger = rg.preprocess(C, EPS, T, self.pre_threads)
+        est_q = max(t_sw * 1.2, 1e-4)  # a query: 4 sweeps with the zero-skip
+        k = int(budget_s * 0.5 / est_q * self.workers)
+        self.qs = int(min(self.nq, max(16, self.workers, k)))
+        self.cursor = 0
+
+    def step(self):
+        rg = self.rg
+        if self.whole_pre:
+            _, t_pre = rg.time_preprocess(C, EPS, T, self.pre_threads)
+            pre_note = f"preprocess() timed whole (threads={self.pre_threads})"
         else:
-            k = max(1, min(3, int(budget_s * 0.3 / max(t_sweep, 1e-9))))
-            t_pre = rg.time_sweeps(k, C, 1) / k * 116
-            stranger = np.zeros(n)
-            pre_note = f"preprocess extrapolated from {k} dense sweeps x 116"
-        # queries: concurrent reference query() calls on all host threads
-        est_q = max(t_sweep * 0.3, 1e-4)
-        nsample = int(max(workers, min(nq, budget_s * 0.4 / est_q * workers)))
-        nsample = min(nq, max(1, nsample))
-        _, t_q = rg.query_many(stranger, C, EPS, T, seeds[:nsample], S, workers)
-        t_job = t_pre + t_q * nq / nsample
-        sample = (f"{pre_note} (threads=1) + {nsample} of {nq} queries on {workers} threads "
-                  f"(reference query(), concurrent), job time extrapolated")
-    else:
-        orc = Oracle()
-        kind = "port"
-        workers = 1
-        t0 = time.perf_counter()
-        stranger = orc.preprocess(g, C, EPS, T)
-        t_pre = time.perf_counter() - t0
-        nsample = min(nq, 8)
-        t0 = time.perf_counter()
-        for s in seeds[:nsample]:
-            orc.query(g, stranger, C, EPS, T, int(s), S)
-        t_q = time.perf_counter() - t0
-        t_job = t_pre + t_q * nq / nsample
-        sample = f"oracle port: preprocess whole + {nsample} of {nq} queries serial, extrapolated"
-    edges = m * (116 + 4 * nq)
-    return {"value": edges / t_job / 1e9, "unit": "GTEPS", "cores": int(workers), "kind": kind,
-            "sample": sample, "job_s": t_job, "preprocess_s": t_pre,
-            "queries_per_s": nq / (t_job - t_pre) if t_job > t_pre else None}
+            t_pre = rg.time_sweeps(1, C, self.pre_threads) * self.sweeps
+            pre_note = (f"preprocess extrapolated: {self.sweeps} x one dense propagation_sweep "
+                        f"(threads={self.pre_threads})")
+        idx = (self.cursor + np.arange(self.qs)) % self.nq
+        self.cursor = int((self.cursor + self.qs) % self.nq)
+        _, t_q = rg.query_many(self.stranger, C, EPS, T, self.seeds[idx], S, self.workers)
+        t_job = t_pre + t_q * self.nq / self.qs
+        return {"job_s": t_job, "preprocess_s": t_pre, "queries_per_s": self.qs / t_q,
+                "sample": f"{pre_note} + {self.qs} of {self.nq} queries as concurrent reference query() "
+                          f"calls on {self.workers} threads; job time extrapolated"}
+
+    def baseline(self, recs):
+        job = statistics.mean(r["job_s"] for r in recs)
+        edges = self.m * (self.sweeps + (S - 1) * self.nq)
+        return {"value": edges / job / 1e9, "unit": "GTEPS", "cores": int(self.workers), "kind": "reference",
+                "cpu_model": cpu_model(), "sample": recs[-1]["sample"], "job_s": job,
+                "preprocess_s": statistics.mean(r["preprocess_s"] for r in recs),
+                "preprocess_threads": self.pre_threads, "sweep_calibration_s": self.t_sweep_cal,
+                "queries_per_s": statistics.mean(r["queries_per_s"] for r in recs), "extrapolated": True}
+
+
+def cpu_measure(rg, seeds, budget_s=20.0):
+    """cpu_baseline of the GPU arm: one bounded reference sample (after an
+    untimed one)."""
+    smp = RefCpuSampler(rg, seeds, budget_s)
+    smp.step()
+    return smp.baseline([smp.step()])
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref, compiled from
+    /root/reference/proj/src) on this box's host cores.  Imports nothing of the
+    product package: graph, seeds and timing all come from the reference build."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg_name = args.config
     _, _, nq, batch, seed = CONFIGS[cfg_name]
-    import paper_1708_02574_b200 as P
-    g = build_graph(cfg_name)
-    seeds = P.sample_seeds(g, nq, seed)
-    vals = []
-    cb = None
-    steps = max(1, args.steps)
-    for i in range(max(0, args.warmup) + steps):
-        budget = 20.0 if i >= args.warmup else 5.0
-        r = cpu_measure(g, seeds, cfg_name, budget_s=budget)
+    t0 = time.perf_counter()
+    rg = reference_graph(cfg_name)
+    t_build = time.perf_counter() - t0
+    log(f"[reference] graph {cfg_name}: n={rg.n} m={rg.m} built in {t_build:.1f}s")
+    seeds = rg.sample_seeds(nq, seed)
+    smp = RefCpuSampler(rg, seeds, budget_s=args.cpu_budget)
+    recs = []
+    for i in range(max(0, args.warmup) + max(1, args.steps)):
+        r = smp.step()
         if i >= args.warmup:
-            vals.append(r["value"])
-            cb = r
-    v = statistics.median(vals)
-    cb = dict(cb, value=v)
+            recs.append(r)
+    cb = smp.baseline(recs)
+    v = cb["value"]
     line = {"impl": "reference", "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",
-            "value": v, "unit": "GTEPS", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+            "value": v, "unit": "GTEPS", "n_gpus": args.gpus, "steps": max(1, args.steps), "warmup": args.warmup,
             "ms_per_step": cb["job_s"] * 1e3, "higher_is_better": True,
             "scaling": "strong" if args.gpus > 1 else "weak",  # one job, as our arm's N > 1 line
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_desc(cfg_name, g, nq, batch), "queries_per_s": cb["queries_per_s"],
-            "cpu_baseline": cb,
+            "config": workload_desc(cfg_name, rg.n, rg.m, len(rg.dangling), rg.fingerprint, nq, batch),
+            "queries_per_s": cb["queries_per_s"], "cpu_baseline": cb, "graph_build_s": t_build,
             "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -627,7 +681,17 @@ def run_ours(args):
         os.sched_setaffinity(0, all_cpus)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_measure(g, seeds, cfg_name, budget_s=args.cpu_budget)
+        from oracle import Reference
+    if rank == 0 and world == 1 and not args.no_cpu and Reference.available():
+        t0 = time.perf_counter()
+        off = g.out_offsets().astype(np.int64)
+        rg = Reference().graph_from_edges(n, np.repeat(np.arange(n, dtype=np.uint32), np.diff(off)),
+                                          g.out_targets(), "selfloop")
+        del off
+        assert rg.fingerprint == g.fingerprint(), "reference graph differs from the product's"
+        log(f"[rank 0] reference graph for cpu_baseline in {time.perf_counter() - t0:.1f}s")
+        cpu = cpu_measure(rg, seeds, budget_s=args.cpu_budget)
+        del rg
 
     if rank == 0:
         line = {
@@ -635,7 +699,7 @@ def run_ours(args):
             "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg_name, g, nq, batch),
+            "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg_name, n, m, len(g.dangling_nodes()), g.fingerprint(), nq, batch),
             "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e if e2e is not None else e2e_topk,
             "e2e_topk": e2e_topk, "gpu_launches": launches,

@@ -151,6 +151,10 @@ class Reference:
             "ref_last_error": ([], C.c_char_p),
             "ref_graph_from_edges": ([C.c_uint32, _u32p, _u32p, C.c_uint64, C.c_int, C.POINTER(vp)], C.c_int),
             "ref_graph_random": ([C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(vp)], C.c_int),
+            "ref_graph_rmat": ([C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int,
+                                C.c_int, C.POINTER(vp)], C.c_int),
+            "ref_sample_seeds": ([vp, C.c_uint64, C.c_uint64, _u32p], C.c_int),
+            "ref_graph_max_indeg": ([vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)], None),
             "ref_graph_free": ([vp], None),
             "ref_graph_n": ([vp], C.c_uint32),
             "ref_graph_m": ([vp], C.c_uint64),
@@ -196,6 +200,13 @@ class Reference:
         self._chk(self.lib.ref_graph_random(n, m, seed, _policy(policy), C.byref(h)))
         return RefGraph(self, h)
 
+    def graph_rmat(self, scale, edge_factor, a=0.57, b=0.19, c=0.19, seed=1, policy="selfloop", threads=0):
+        """The benchmark R-MAT graph built by the reference Graph constructor
+        (ref_capi.cpp ref_graph_rmat; same edges as the product's generator)."""
+        h = C.c_void_p()
+        self._chk(self.lib.ref_graph_rmat(scale, edge_factor, a, b, c, seed, _policy(policy), threads, C.byref(h)))
+        return RefGraph(self, h)
+
 
 class RefGraph:
     """A reference rwrank::Graph living in the reference library."""
@@ -224,6 +235,17 @@ class RefGraph:
     @property
     def policy(self):
         return self._policy
+
+    def sample_seeds(self, count, rng_seed):
+        """rwrank_main.cpp:65-83 restated (ref_capi.cpp ref_sample_seeds)."""
+        out = np.empty(count, np.uint32)
+        self.ref._chk(self.ref.lib.ref_sample_seeds(self.h, count, rng_seed, out))
+        return out
+
+    def max_indeg(self):
+        node, deg = C.c_uint32(), C.c_uint64()
+        self.ref.lib.ref_graph_max_indeg(self.h, C.byref(node), C.byref(deg))
+        return node.value, deg.value
 
     def sweep(self, x, c, threads=1):
         y = np.empty(self.n, np.float64)

@@ -10,11 +10,13 @@
 // status codes with the message kept per thread:
 //   0 ok, 1 std::invalid_argument, 2 std::out_of_range, 3 std::runtime_error,
 //   5 anything else.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -80,6 +82,130 @@ int ref_graph_from_edges(uint32_t n, const uint32_t* src, const uint32_t* dst, u
 
 int ref_graph_random(uint32_t n, uint64_t m, uint64_t seed, int policy, void** out) {
     return guard([&] { *out = new Graph(rwrank::generate_random_graph(n, m, seed, pol(policy))); });
+}
+
+// The benchmark's R-MAT generator (BASELINE.json configs C1/C2/C4/C5), restated
+// here so the reference arm and the fixture scripts build their graph without
+// the product library: edge e is drawn from the mt19937_64 stream of its
+// 2^20-edge chunk, seeded (seed * 0x9E3779B97F4A7C15 + chunk * 0xD1B54A32D192ED03 + 1);
+// per level one 53-bit uniform picks quadrant (0,0) a, (0,1) b, (1,0) c, (1,1)
+// rest, MSB first; self-loops are dropped.  The edges are pre-sorted and
+// de-duplicated per source on all host threads, then handed to the
+// reference's own Graph constructor (graph.cpp:53-91), which sorts, dedupes,
+// repairs and fingerprints them itself -- the pre-sort only spares its
+// single-threaded std::sort the random input.
+int ref_graph_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                   uint64_t seed, int policy, int threads, void** out) {
+    return guard([&] {
+        if (scale == 0 || scale > 31) throw std::invalid_argument("rmat scale must be in [1, 31]");
+        const uint64_t n = uint64_t(1) << scale, m = n * edge_factor;
+        constexpr uint64_t kChunk = 1u << 20;
+        const uint64_t nchunks = (m + kChunk - 1) / kChunk;
+        const unsigned T = threads > 0 ? unsigned(threads) : std::max(1u, std::thread::hardware_concurrency());
+        std::vector<uint32_t> u(m), v(m);
+        const double ab = a + b, abc = a + b + c;
+        {
+            std::atomic<uint64_t> next{0};
+            std::vector<std::thread> pool;
+            for (unsigned k = 0; k < T; ++k)
+                pool.emplace_back([&] {
+                    for (uint64_t ch = next++; ch < nchunks; ch = next++) {
+                        std::mt19937_64 rng(seed * 0x9E3779B97F4A7C15ULL + ch * 0xD1B54A32D192ED03ULL + 1);
+                        const uint64_t e1 = std::min(m, (ch + 1) * kChunk);
+                        for (uint64_t e = ch * kChunk; e < e1; ++e) {
+                            uint32_t x = 0, y = 0;
+                            for (uint32_t lvl = 0; lvl < scale; ++lvl) {
+                                const double r = double(rng() >> 11) * 0x1.0p-53;
+                                const uint32_t bit = 1u << (scale - 1 - lvl);
+                                if (r < a) {
+                                } else if (r < ab) {
+                                    y |= bit;
+                                } else if (r < abc) {
+                                    x |= bit;
+                                } else {
+                                    x |= bit;
+                                    y |= bit;
+                                }
+                            }
+                            u[e] = x;
+                            v[e] = y;
+                        }
+                    }
+                });
+            for (auto& t : pool) t.join();
+        }
+        // counting sort by source (serial counts, parallel per-source sorts)
+        std::vector<uint64_t> off(n + 1, 0);
+        for (uint64_t e = 0; e < m; ++e)
+            if (u[e] != v[e]) ++off[u[e] + 1];
+        for (uint64_t i = 0; i < n; ++i) off[i + 1] += off[i];
+        std::vector<uint32_t> bucket(off[n]);
+        {
+            std::vector<uint64_t> cur(off.begin(), off.end() - 1);
+            for (uint64_t e = 0; e < m; ++e)
+                if (u[e] != v[e]) bucket[cur[u[e]]++] = v[e];
+        }
+        u.clear();
+        u.shrink_to_fit();
+        v.clear();
+        v.shrink_to_fit();
+        std::vector<uint64_t> deg(n, 0);
+        {
+            std::vector<std::thread> pool;
+            for (unsigned k = 0; k < T; ++k)
+                pool.emplace_back([&, k] {
+                    for (uint64_t x = n * k / T; x < n * (k + 1) / T; ++x) {
+                        uint32_t* lo = bucket.data() + off[x];
+                        uint32_t* hi = bucket.data() + off[x + 1];
+                        std::sort(lo, hi);
+                        deg[x] = uint64_t(std::unique(lo, hi) - lo);
+                    }
+                });
+            for (auto& t : pool) t.join();
+        }
+        uint64_t kept = 0;
+        for (uint64_t x = 0; x < n; ++x) kept += deg[x];
+        std::vector<std::pair<NodeId, NodeId>> edges;
+        edges.reserve(kept + n / 2);  // room for the SelfLoop repair edges
+        for (uint64_t x = 0; x < n; ++x)
+            for (uint64_t i = 0; i < deg[x]; ++i) edges.emplace_back(NodeId(x), bucket[off[x] + i]);
+        std::vector<uint32_t>().swap(bucket);
+        *out = new Graph(NodeId(n), std::move(edges), pol(policy));
+    });
+}
+
+// sample_seeds (tools/rwrank_main.cpp:65-83, the CLI's seed sampler; not part
+// of the library): uniform without replacement over non-dangling nodes.
+int ref_sample_seeds(void* gp, uint64_t count, uint64_t rng_seed, uint32_t* out) {
+    return guard([&] {
+        const Graph& g = *static_cast<Graph*>(gp);
+        std::vector<bool> dangling(g.node_count(), false);
+        for (NodeId x : g.dangling_nodes()) dangling[x] = true;
+        std::vector<NodeId> pool;
+        pool.reserve(g.node_count());
+        for (NodeId x = 0; x < g.node_count(); ++x)
+            if (!dangling[x]) pool.push_back(x);
+        if (pool.size() < count)
+            throw std::runtime_error("graph has only " + std::to_string(pool.size()) +
+                                     " non-dangling nodes; cannot draw " + std::to_string(count) +
+                                     " seeds");
+        std::mt19937_64 rng(rng_seed);
+        for (std::size_t i = 0; i < count; ++i) {
+            std::uniform_int_distribution<std::size_t> pick(i, pool.size() - 1);
+            std::swap(pool[i], pool[pick(rng)]);
+        }
+        std::memcpy(out, pool.data(), count * 4);
+    });
+}
+
+// max in-degree node of the graph and its in-degree (test helper)
+void ref_graph_max_indeg(void* gp, uint32_t* node, uint64_t* indeg) {
+    const Graph& g = *static_cast<Graph*>(gp);
+    std::vector<uint64_t> d(g.node_count(), 0);
+    for (NodeId t : g.out_targets()) ++d[t];
+    const auto it = std::max_element(d.begin(), d.end());
+    *node = NodeId(it - d.begin());
+    *indeg = *it;
 }
 
 void ref_graph_free(void* g) { delete static_cast<Graph*>(g); }

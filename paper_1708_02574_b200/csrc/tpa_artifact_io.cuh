@@ -255,6 +255,11 @@ int tpa_artifact_load(tpa_graph* g, const char* path, tpa_artifact** out) {
         if (version != kArtifactVersion)
             throw std::runtime_error("unsupported artifact version " + std::to_string(version));
         const uint64_t n = get_le(pinned + 8, 8);
+        // node ids are uint32 (graph.hpp NodeId); a larger count is corrupt and
+        // would wrap 48 + 8n
+        if (n > 0xffffffffull)
+            throw std::runtime_error("artifact truncated or oversized: node count " + std::to_string(n) +
+                                     " exceeds the uint32 node-id range");
         const uint64_t expected = 48 + 8 * n;
         if (size != expected)
             throw std::runtime_error("artifact truncated or oversized: expected " + std::to_string(expected) +

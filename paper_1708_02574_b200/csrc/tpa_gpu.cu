@@ -156,29 +156,57 @@ __global__ void k_row_ptr(const uint32_t* __restrict__ keys, uint64_t m, uint32_
 __global__ void __launch_bounds__(kThreads)
 k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
              const uint32_t* __restrict__ deg, double keep, double* __restrict__ share0,
-             double* __restrict__ acc0, unsigned long long* fx) {
+             double* __restrict__ acc0, unsigned long long* fx, double* __restrict__ dm_part) {
     __shared__ unsigned long long s_w[4 * (kThreads / 32)];
+    __shared__ double s_dm[kThreads / 32];
     unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+    double sdm = 0.0;
     for (uint64_t u = blockIdx.x * (uint64_t)kThreads + threadIdx.x; u < n; u += (uint64_t)gridDim.x * kThreads) {
         const double xv = x ? x[u] : weight;
         const uint32_t d = deg[u];
         share0[u] = d ? ddiv(dmul(keep, xv), (double)d) : 0.0;
         if (acc0) acc0[u] = xv;
         fx_add(f0, f1, xv);
-        if (d == 0) fx_add(f2, f3, xv);
+        if (d == 0) {
+            if (dm_part) sdm = dadd(sdm, xv);
+            else fx_add(f2, f3, xv);
+        }
+    }
+    if (dm_part) {
+        // a caller-supplied x (propagation_sweep): any sign and magnitude, so the
+        // dangling mass is a signed double sum (graph.cpp:213-225 sums signed
+        // doubles) in a fixed order -- grid-stride per thread, a fixed warp tree,
+        // warps in order, blocks in order (k_init_finish)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sdm = dadd(sdm, __shfl_down_sync(0xffffffffu, sdm, o));
+        if ((threadIdx.x & 31) == 0) s_dm[threadIdx.x >> 5] = sdm;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = s_dm[0];
+            for (int k = 1; k < kThreads / 32; ++k) t = dadd(t, s_dm[k]);
+            dm_part[blockIdx.x] = t;
+        }
     }
     fx_cta_flush(f0, f1, f2, f3, s_w, fx);
 }
 
 // x⁰'s ColState from the totals (then fx is zeroed for the sweeps); a
 // partition instead publishes limbs for the all-reduce + k_part_finalize.
+// dm_part (n_parts block sums, in block order) replaces the fixed-point
+// dangling total when the start vector was caller-supplied.
 __global__ void k_init_finish(unsigned long long* fx, unsigned long long* limbs, int policy, double keep,
-                              uint32_t n, int active0, ColState* state0) {
+                              uint32_t n, int active0, ColState* state0, const double* dm_part,
+                              int n_parts) {
     if (limbs) {
         fx_to_limbs(fx[0], fx[1], limbs);
         fx_to_limbs(fx[2], fx[3], limbs + 3);
     } else {
-        const double l1 = fx_decode(fx[0], fx[1]), dm = fx_decode(fx[2], fx[3]);
+        const double l1 = fx_decode(fx[0], fx[1]);
+        double dm = fx_decode(fx[2], fx[3]);
+        if (dm_part) {
+            dm = dm_part[0];
+            for (int k = 1; k < n_parts; ++k) dm = dadd(dm, dm_part[k]);
+        }
         ColState s;
         s.residual = l1;
         s.iters = 0;
@@ -461,6 +489,7 @@ struct Workspace {
     DevBuf big;                  // sparse sweeps: edge chunks of high out-degree frontier rows
     DevBuf limbs;                // partition mode: [3][6] fixed-point limbs (sweep parity 0/1, init) + [6] totals
     DevBuf sl;                   // sparse sweeps: segments of the marked long rows
+    DevBuf dm_part;              // caller-supplied x: per-block signed dangling sums
     int grid_gather = 0, grid_epi = 0;
 };
 
@@ -715,6 +744,7 @@ struct RunCfg {
     int64_t terminal = -1;
     Init init = Init::Dense;
     const double* d_x = nullptr;     // Dense: explicit x⁽⁰⁾ (null -> uniform weight)
+    bool signed_x = false;           // d_x caller-supplied (any sign / magnitude): signed dangling sum
     double weight = 0.0;             // Dense with d_x == null
     SeedList seeds{};                // Seeds (by value)
     // accumulation: windowed single acc, or partition segment accs
@@ -1018,12 +1048,17 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int active0 = cfg.terminal != 0;
     if (cfg.init == Init::Dense) {
         const int nblk = grid_for(n, 4 * kThreads, 4 * g->num_sms);
+        double* dm_part = nullptr;
+        if (cfg.signed_x) {
+            w.dm_part.ensure((size_t)nblk * 8, g->stream);
+            dm_part = w.dm_part.as<double>();
+        }
         k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.d_x, cfg.weight, n, deg_run, keep,
                                                        w.share[0].as<double>(), acc0,
-                                                       w.fx.as<unsigned long long>());
+                                                       w.fx.as<unsigned long long>(), dm_part);
         CKL("k_init_dense");
         k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), nullptr, g->policy, keep, n,
-                                              active0, st);
+                                              active0, st, dm_part, nblk);
         CKL("k_init_finish");
         g->launches += 2;
     } else if (mm) {
@@ -1643,6 +1678,7 @@ int tpa_propagation_sweep(tpa_graph* g, const double* x, double* y, double c, in
         cfg.terminal = 1;
         cfg.init = Init::Dense;
         cfg.d_x = xd;
+        cfg.signed_x = true;
         cfg.y_out = yd;
         cfg.want_state = false;
         // c == 0 is legal for a sweep; the driver only uses keep = 1 - c.

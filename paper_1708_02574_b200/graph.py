@@ -213,15 +213,33 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def vec_ptr(x, count=None, dtype=np.float64):
-    """(pointer, is_device, keepalive) for a numpy array or torch tensor."""
+def vec_ptr(x, count=None, dtype=np.float64, writable=False, device=None):
+    """(pointer, is_device, keepalive) for a numpy array or torch tensor.
+
+    Tensors must be contiguous, of exactly `dtype` and, when on a GPU, on
+    `device` (the graph's).  A numpy *input* may be converted (a copy); an
+    output (`writable`) must already be a C-contiguous, writeable array of
+    `dtype` -- results are written straight into it, never into a temporary."""
     if _is_torch(x):
+        import torch
+        want = {np.dtype(np.float64): torch.float64, np.dtype(np.uint32): torch.int32,
+                np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+        if x.dtype != want:
+            raise TypeError(f"tensor must be {want}, got {x.dtype}")
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
         if count is not None and x.numel() != count:
             raise ValueError("score vector length does not match node count")
+        if x.is_cuda and device is not None and x.device.index != int(device):
+            raise ValueError(f"tensor is on cuda:{x.device.index}, the graph on cuda:{int(device)}")
         return x.data_ptr(), x.is_cuda, x
-    a = np.ascontiguousarray(x, dtype)
+    if writable:
+        if not isinstance(x, np.ndarray) or x.dtype != np.dtype(dtype) or not x.flags.c_contiguous \
+                or not x.flags.writeable:
+            raise ValueError(f"output must be a writeable C-contiguous {np.dtype(dtype)} array")
+        a = x
+    else:
+        a = np.ascontiguousarray(x, dtype)
     if count is not None and a.size != count:
         raise ValueError("score vector length does not match node count")
     return a.ctypes.data, False, a
@@ -285,16 +303,18 @@ def propagation_sweep(g: Graph, x, c: float, threads: int = 1, out=None):
     """graph.hpp:96-103: y = (1-c)·Ãᵀx (+ dangling term), on the GPU.
     ``threads`` is accepted for signature parity and ignored."""
     n = g.node_count()
-    xp, xdev, keep_x = vec_ptr(x, n)
+    xdev0 = _is_torch(x) and x.is_cuda
+    dev = x.device.index if xdev0 else 0
+    xp, xdev, keep_x = vec_ptr(x, n, device=dev)
     if out is None:
         if xdev:
             import torch
             out = torch.empty(n, dtype=torch.float64, device=x.device)
         else:
             out = np.empty(n, np.float64)
-    yp, ydev, keep_y = vec_ptr(out, n)
+    yp, ydev, keep_y = vec_ptr(out, n, writable=True, device=dev)
     if xdev != ydev:
         raise ValueError("x and y must both be host or both be device vectors")
-    check(lib.tpa_propagation_sweep(g.device(x.device.index if xdev else 0).h, xp, yp, float(c),
+    check(lib.tpa_propagation_sweep(g.device(dev).h, xp, yp, float(c),
                                     N.TPA_DEVICE_PTRS if xdev else 0))
     return out

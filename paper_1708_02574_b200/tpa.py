@@ -151,7 +151,7 @@ def exact_rwr_batch(g: Graph, seeds, c: float = kDefaultRestartProb, eps: float 
     n = g.node_count()
     if out is None:
         out = np.empty((s.size, n), np.float64)
-    p, dev, keep = vec_ptr(out, s.size * n)
+    p, dev, keep = vec_ptr(out, s.size * n, writable=True, device=_dev(g).device)
     check(lib.tpa_exact_rwr_batch(_dev(g).h, s.ctypes.data, s.size, float(c), float(eps), p,
                                   N.TPA_DEVICE_PTRS if dev else 0))
     return out
@@ -178,7 +178,10 @@ class TpaParams:
 
 @dataclass(eq=False)
 class StrangerArtifact:
-    """tpa.hpp:17-23 (+ a cached device copy of the stranger vector)."""
+    """tpa.hpp:17-23 (+ a cached device copy of the stranger vector).
+
+    Once uploaded, ``stranger_scores`` is read-only (the device copy is keyed
+    by the array object); assign a new array to change the scores."""
     stranger_scores: np.ndarray = field(default_factory=lambda: np.empty(0))
     graph_fingerprint: int = 0
     restart_prob: float = kDefaultRestartProb
@@ -205,7 +208,15 @@ class StrangerArtifact:
         check(lib.tpa_artifact_create(dg.h, st.ctypes.data, int(self.graph_fingerprint), float(self.restart_prob),
                                       float(self.tolerance), int(self.stranger_start), 0, C.byref(h)))
         self._dev = (dg, self._key(), h)
+        self._freeze()
         return h
+
+    def _freeze(self):
+        # the device copy follows the array's identity (_key): freeze the
+        # uploaded array so an in-place edit cannot leave a stale device copy
+        # -- assign a new array to change the scores (it is re-uploaded)
+        if isinstance(self.stranger_scores, np.ndarray):
+            self.stranger_scores.flags.writeable = False
 
     def _release(self):
         if self._dev is not None:
@@ -229,6 +240,7 @@ def preprocess(g: Graph, c: float, eps: float, stranger_start: int, threads: int
     check(lib.tpa_preprocess(dg.h, float(c), float(eps), int(stranger_start), out.ctypes.data, C.byref(h), 0))
     art = StrangerArtifact(out, g.fingerprint(), float(c), float(eps), int(stranger_start))
     art._dev = (dg, art._key(), h)
+    art._freeze()
     return art
 
 
@@ -290,7 +302,7 @@ def query_batch(g: Graph, artifact: StrangerArtifact, seeds, family_end: int, ou
     sp = s.ctypes.data
     if out is None:
         out = np.empty((B, n) if not node_major else (n, B), np.float64)
-    p, odev, keep = vec_ptr(out, B * n)
+    p, odev, keep = vec_ptr(out, B * n, writable=True, device=dg.device)
     flags = (N.TPA_DEVICE_PTRS if odev else 0) | (N.TPA_NODE_MAJOR if node_major else 0) | \
             (N.TPA_QUERY_NA if na else 0) | (N.TPA_ASYNC if (odev and not sync) else 0)
     check(lib.tpa_query_batch(dg.h, artifact.device(g), sp, B, int(family_end), p, flags))

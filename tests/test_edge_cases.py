@@ -68,3 +68,27 @@ def test_every_node_dangling_but_one(oracle):
     for policy in POLICIES:
         g = P.Graph(50, [(3, 4)], policy)
         _check(oracle, g, np.array([3, 4, 0, 49], np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", POLICIES)
+def test_sweep_of_caller_vectors(oracle, policy):
+    """propagation_sweep (graph.cpp:230-270) of arbitrary caller vectors: a
+    dangling entry far above any CPI mass, x = ones over hundreds of dangling
+    nodes (dangling mass >= 256), and signed entries -- the Uniform spread is a
+    signed sum of the dangling entries (a clamped fixed-point total
+    got these wrong)."""
+    g = P.Graph(3, [(0, 1)], policy)  # nodes 1 and 2 dangling
+    x = np.array([0.0, 100.0, 0.0])
+    assert_close(P.propagation_sweep(g, x, C), oracle.sweep(g, x, C), max_abs=1e-13, what="x = 100 e_1")
+    rng = np.random.default_rng(5)
+    n = 2000
+    src = rng.integers(0, n // 2, 6000, dtype=np.uint32)  # nodes >= n/2 dangling
+    dst = rng.integers(0, n, 6000, dtype=np.uint32)
+    g = P.Graph(n, (src, dst), policy)
+    for x, what in ((np.ones(n), "ones"), (rng.normal(0.0, 50.0, n), "signed"),
+                    (np.where(np.arange(n) % 2 == 0, 1e3, -1e3), "alternating")):
+        want = oracle.sweep(g, x, C)
+        # entries are O(1e3) here: the bar scales with them (relative 1e-15)
+        bar = 1e-15 * max(1.0, np.abs(x).sum())
+        assert_close(P.propagation_sweep(g, x, C), want, max_abs=bar, l1=bar * n, what=what)

@@ -154,3 +154,27 @@ def test_param_validation_like_reference():
     t.family_end, t.stranger_start = 5, 5
     with pytest.raises(ValueError):
         t.validate()
+
+
+def test_vec_ptr_rejects_bad_buffers():
+    """Outputs must be written in place: wrong dtype, non-contiguous or read-only
+    outputs and wrong-dtype tensors are refused, never copied."""
+    import torch
+    from paper_1708_02574_b200.graph import vec_ptr
+    with pytest.raises(TypeError):
+        vec_ptr(torch.zeros(8, dtype=torch.float32), 8)
+    with pytest.raises(ValueError):
+        vec_ptr(np.zeros(8, np.float32), 8, writable=True)
+    with pytest.raises(ValueError):
+        vec_ptr(np.zeros(16)[::2], 8, writable=True)
+    ro = np.zeros(8)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        vec_ptr(ro, 8, writable=True)
+    with pytest.raises(ValueError):
+        vec_ptr(np.zeros(9), 8, writable=True)
+    a = np.zeros(8)
+    p, dev, keep = vec_ptr(a, 8, writable=True)
+    assert p == a.ctypes.data and not dev and keep is a
+    p, dev, keep = vec_ptr([1, 2, 3], 3)  # inputs may be converted
+    assert keep.dtype == np.float64

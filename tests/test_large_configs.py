@@ -1,0 +1,133 @@
+"""Full-size parity at BASELINE.json configs[2] (C3, ER 4.2 M / 67 M edges) and
+configs[3] (C4, R-MAT 24, 529 M edges) -- the bench headline's graph.
+
+Pinned two ways:
+* against the UNMODIFIED reference at threads = 1, through the committed
+  fixtures tests/golden/large/<config>.npz (oracle/make_large_fixtures.py:
+  graph identity, the stranger vector's iteration count / residual / L1 norm /
+  values at 20k sampled ids / top-1000, and four reference query() results as
+  L1 norm, sampled values and top-100);
+* element-wise against the C oracle at run time: PageRank window [0, 3] and
+  the four fixture queries (one seeded at an in-neighbour of the
+  max-in-degree node, so the longest CSR(A^T) row is live from sweep 1),
+  taken from a B-wide batch at different slots.
+Plus the closed-form mass of EVERY query of the config's job (SelfLoop keeps
+mass: ||query||_1 = (1+nsf)(1-(1-c)^S) + ||stranger||_1, within eps/c).
+
+Matches tpa.cpp:19-37 (preprocess), :61-76 (query), cpi.cpp:55-83 (run_series).
+"""
+from __future__ import annotations
+
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, MAX_ABS, assert_close
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+P = pytest.importorskip("paper_1708_02574_b200")
+C, EPS, S, T = 0.15, 1e-9, 5, 10
+JOBS = {"c3": (4096, 64), "c4": (1024, 32)}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _graph(cfg):
+    if cfg == "c3":
+        return P.generate_random_graph(4194304, 67108864, 1)
+    return P.generate_rmat(24, 32, 0.57, 0.19, 0.19, rng_seed=1, device=0)
+
+
+def _top(v, k):
+    cand = np.argpartition(-v, k + 64)[:k + 64]
+    order = np.lexsort((cand, -v[cand]))  # score desc, ties by ascending id (metrics.cpp:25-36)
+    return cand[order][:k]
+
+
+def _check_top(got_vec, want_ids, want_vals, what):
+    """top-k equal to the reference's up to ties closer than the parity bar."""
+    k = len(want_ids)
+    ids = _top(got_vec, k)
+    assert np.max(np.abs(got_vec[ids] - want_vals)) <= MAX_ABS, what
+    assert np.max(np.abs(got_vec[want_ids.astype(np.int64)] - want_vals)) <= MAX_ABS, what
+    differ = ids != want_ids
+    if differ.any():  # only inside runs of (near-)equal scores
+        gaps = np.abs(np.diff(want_vals))
+        for i in np.nonzero(differ)[0]:
+            near = (i > 0 and gaps[i - 1] <= MAX_ABS) or (i < k - 1 and gaps[i] <= MAX_ABS)
+            assert near, f"{what}: rank {i} id {ids[i]} vs reference {want_ids[i]}"
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_config_full(cfg, oracle):
+    import torch
+    fx = dict(np.load(os.path.join(GOLDEN, "large", f"{cfg}.npz")))
+    t0 = time.perf_counter()
+    g = _graph(cfg)
+    n, m = g.node_count(), g.edge_count()
+    print(f"{cfg}: n={n} m={m} built in {time.perf_counter() - t0:.1f}s")
+    # the same graph as the reference's (its Graph constructor, graph.cpp:53-91)
+    assert (n, m, len(g.dangling_nodes())) == (int(fx["n"]), int(fx["m"]), int(fx["n_dangling"]))
+    assert g.fingerprint() == int(fx["fingerprint"])
+
+    pool = ThreadPoolExecutor(4)  # the oracle runs on host cores while the GPU works
+    w3 = pool.submit(oracle.pagerank, g, C, EPS, 0, 3)
+
+    # PageRank window [0, 3] (cpi_run), element-wise against the oracle
+    pr3 = P.cpi_run(g, P.SeedSet.all_nodes(n), P.CpiParams(C, EPS, 0, 3))
+    # the full preprocess: 116 sweeps, window [T, inf)
+    art = P.preprocess(g, C, EPS, T)
+    pr = P.pagerank(g, P.CpiParams(C, EPS, T))
+    st = art.stranger_scores
+    assert pr.iterations_run == int(fx["pr_iterations"]) == 116
+    assert pr.converged == bool(fx["pr_converged"])
+    assert abs(pr.residual_l1 - float(fx["pr_residual"])) <= 1e-15
+    assert_close(pr.scores, st, what=f"{cfg} pagerank(start T) vs preprocess")
+    ids = fx["ids"].astype(np.int64)
+    d = np.abs(st[ids] - fx["stranger_at"])
+    assert d.max() <= MAX_ABS, f"{cfg} stranger at sampled ids: max-abs {d.max():.3e}"
+    assert abs(np.abs(st).sum() - float(fx["stranger_l1"])) <= 1e-9
+    _check_top(st, fx["stranger_top_ids"], fx["stranger_top_vals"], f"{cfg} stranger top-1000")
+
+    # the four fixture queries inside one batch, at slots 0, 5, B/2, B-1
+    nq, B = JOBS[cfg]
+    draw = P.sample_seeds(g, nq, 1)
+    qs = fx["query_seeds"].astype(np.uint32)
+    assert draw[0] == qs[0] and draw[1] == qs[1] and draw[-1] == qs[3]
+    batch = draw[:B].copy()
+    slots = [0, 5, B // 2, B - 1]
+    batch[slots] = qs
+    out = torch.empty((B, n), dtype=torch.float64, device="cuda")
+    P.query_batch(g, art, batch, S, out=out)
+    host = out.cpu().numpy()
+    wq = [pool.submit(oracle.query, g, st, C, EPS, T, int(s), S) for s in qs]
+    for k, s in enumerate(qs):
+        got = host[slots[k]]
+        assert_close(got, wq[k].result(), what=f"{cfg} query seed {s} (slot {slots[k]}) vs oracle")
+        d = np.abs(got[ids] - fx["query_at"][k])
+        assert d.max() <= MAX_ABS, f"{cfg} query {s} at sampled ids vs reference: {d.max():.3e}"
+        assert abs(np.abs(got).sum() - float(fx["query_l1"][k])) <= 1e-9
+        _check_top(got, fx["query_top_ids"][k], fx["query_top_vals"][k], f"{cfg} query {s} top-100")
+    # the single-query path on the hub seed
+    assert_close(P.query(g, art, int(qs[2]), S), host[slots[2]], what=f"{cfg} query() vs query_batch")
+    w = w3.result()
+    assert_close(pr3.scores, w[0], what=f"{cfg} pagerank window [0,3]")
+    assert pr3.iterations_run == w[1] == 3
+
+    # every query of the bench job: closed-form mass
+    nsf = P.neighbor_scale_factor(C, S, T)
+    mass = (1 + nsf) * (1 - (1 - C) ** S) + float(st.sum())
+    for b0 in range(0, nq, B):
+        P.query_batch(g, art, draw[b0:b0 + B], S, out=out)
+        sums = out.sum(dim=1).cpu().numpy()
+        assert np.all(np.abs(sums - mass) <= EPS / C), (cfg, b0, sums.min(), sums.max())
+    pool.shutdown()

@@ -10,11 +10,12 @@
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import pytest
 
-from conftest import CsrGraph, golden_files, load_golden
+from conftest import GOLDEN, CsrGraph, golden_files, load_golden
 
 
 @pytest.mark.parametrize("path", golden_files(), ids=lambda p: p.rsplit("/", 1)[-1])
@@ -122,3 +123,33 @@ def test_self_loop_query_is_unit(oracle):
     st = oracle.preprocess(g, 0.15, 1e-9, 10)
     r = oracle.query(g, st, 0.15, 1e-9, 10, 0, 5)
     assert abs(r[0] - 1.0) < 1e-6 * 2
+
+
+def test_reference_side_generator_matches_the_product(reference):
+    """The reference arm and the large fixtures build the benchmark graph with
+    the reference's own Graph constructor from oracle/ref_capi.cpp's R-MAT
+    restatement (no product code): same graph, fingerprint and seed draw as the
+    product's generator (csrc/host_graph.cpp)."""
+    import paper_1708_02574_b200 as P
+    for scale, ef, policy in ((10, 16, "selfloop"), (13, 8, "uniform"), (12, 4, "drop")):
+        g = P.generate_rmat(scale, ef, 0.57, 0.19, 0.19, rng_seed=3, policy=policy)
+        rg = reference.graph_rmat(scale, ef, 0.57, 0.19, 0.19, seed=3, policy=policy)
+        assert rg.fingerprint == g.fingerprint()
+        assert np.array_equal(rg.out_offsets, g.out_offsets()) and np.array_equal(rg.out_targets, g.out_targets())
+        assert np.array_equal(rg.sample_seeds(40, 9), P.sample_seeds(g, 40, 9))
+
+
+def test_large_fixtures_are_consistent():
+    """tests/golden/large/*.npz (oracle/make_large_fixtures.py): the reference's
+    stranger vector and queries obey the SelfLoop closed forms."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(GOLDEN, "large", "*.npz")))
+    assert paths
+    for p in paths:
+        fx = dict(np.load(p))
+        assert int(fx["pr_iterations"]) == 116 and bool(fx["pr_converged"])
+        assert abs(float(fx["stranger_l1"]) - 0.85 ** 10) <= 1e-9 / 0.15
+        nsf = (0.85 ** 5 - 0.85 ** 10) / (1 - 0.85 ** 5)
+        mass = (1 + nsf) * (1 - 0.85 ** 5) + float(fx["stranger_l1"])
+        assert np.all(np.abs(fx["query_l1"] - mass) <= 1e-9 / 0.15)
+        assert np.all(np.diff(fx["stranger_top_vals"]) <= 0)
