@@ -547,17 +547,13 @@ def run_ours(args):
         # dominant kernel: the SpMM sweep.  Roofline on its densest launch, the
         # last family sweep x^(S-1) (fused combine), with that sweep's exact
         # compulsory bytes; the sparse early sweeps are listed per index.
-        ver = os.environ.get("TPA_SPMM", "5") if Bk in (16, 32, 64) else "2"
-        if Bk == 16 and ver != "2":
-            ver = "5"
-        kname = {"5": f"k_mm_fused<{Bk}>", "4": f"k_mm_gather<{Bk}> + k_mm_epi<{Bk}>",
-                 "3": f"k_step_spmm3<{Bk}>"}.get(ver, f"k_step_spmm2<{Bk}>")
+        kname = f"k_mm_fused<{Bk}>" if Bk >= 16 else f"k_step_spmm2<{Bk}>"
         last = per_sweep.get(S - 1)
         bytes_launch = sweep_bytes(n, m, Bk, "last")
         avg_ms = last["avg_ms"] if last else mm_ms / mm_cnt
         share = mm_ms / prof_total_ms if prof_total_ms else None
     else:
-        kname = "k_step_spmv2" if os.environ.get("TPA_SPMV", "2") == "2" else "k_step_spmv"
+        kname = "k_step_spmv2"
         bytes_launch = a_step(n, m, 1, 1)
         avg_ms = mv_ms / max(mv_cnt, 1)
         share = mv_ms / prof_total_ms if prof_total_ms else None

@@ -9,8 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-# TPA_LIB may point at an alternative in-tree build (used for A/B kernel experiments)
-LIB_PATH = os.environ.get("TPA_LIB") or os.path.join(PKG, "libtpa_gpu.so")
+LIB_PATH = os.path.join(PKG, "libtpa_gpu.so")
 
 TPA_OK = 0
 TPA_ERR_INVALID_ARGUMENT = 1

@@ -239,135 +239,6 @@ __device__ __forceinline__ void combine_only(const StepArgs& a, uint32_t v, uint
 }
 
 // ---------------------------------------------------------------------------
-// K2: fused CPI sweep, B = 1 (PageRank / single-vector cpi_run / query()).
-// One CTA per work item: a tile of consecutive short rows (<= kMvTileNnz nnz)
-// staged through shared memory, or one long row reduced by the whole CTA.
-// ---------------------------------------------------------------------------
-constexpr size_t kMv1DynSmem = (size_t)kMvTileNnz * 8 + (kMvTileRows + 1) * 8 + (size_t)kMvTileRows * 8;
-__global__ void __launch_bounds__(kThreads) k_step_spmv(StepArgs a) {
-    extern __shared__ __align__(16) unsigned char s_mv1[];  // kMvTileNnz + 2 kMvTileRows + 1 words
-    double* s_vals = reinterpret_cast<double*>(s_mv1);
-    int64_t* s_rp = reinterpret_cast<int64_t*>(s_vals + kMvTileNnz);
-    double* s_y = reinterpret_cast<double*>(s_rp + kMvTileRows + 1);
-    __shared__ double s_red[kThreads];
-    __shared__ double s_fin[kThreads];
-    __shared__ double s_part[2];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t item = blockIdx.x;
-    const ColState st = a.state_in[0];
-    const uint2 it = a.items[item];
-    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
-    const bool is_long = (it.y & kLongFlag) != 0;
-
-    if (!st.active) {
-        // Column stopped earlier: only a pending combine remains (tpa.cpp:73).
-        if (a.out)
-            for (uint32_t v = rb + tid; v < re; v += kThreads) combine_only(a, v, 0, 1, v);
-        if (item == 0 && tid == 0) a.state_out[0] = st;
-        return;
-    }
-
-    double my_l1 = 0.0, my_dm = 0.0;
-    const bool want_dm = a.policy == kUniform;
-
-    if (!is_long) {
-        const uint32_t nrows = re - rb;
-        for (uint32_t r = tid; r <= nrows; r += kThreads) s_rp[r] = a.row_ptr[rb + r];
-        __syncthreads();
-        const int64_t nb = s_rp[0];
-        const int nnz = (int)(s_rp[nrows] - nb);
-        // Gather: coalesced index loads, 8 independent gathers in flight per thread.
-        {
-            constexpr int U = kMvTileNnz / kThreads;
-            uint32_t u[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int k = tid + j * kThreads;
-                u[j] = k < nnz ? ld_stream_u32(a.col + nb + k) : 0u;
-            }
-            double v[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int k = tid + j * kThreads;
-                v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                const int k = tid + j * kThreads;
-                if (k < nnz) s_vals[k] = v[j];
-            }
-        }
-        __syncthreads();
-        // Short rows: one thread, ascending-source sequential sum (reference order).
-        for (uint32_t r = tid; r < nrows; r += kThreads) {
-            const int lo = (int)(s_rp[r] - nb), hi = (int)(s_rp[r + 1] - nb);
-            if (hi - lo <= kMvShortRow) {
-                double s = 0.0;
-                for (int k = lo; k < hi; ++k) s = dadd(s, s_vals[k]);
-                s_y[r] = s;
-            }
-        }
-        // Longer rows of the tile: one warp each, lane-strided + butterfly.
-        for (uint32_t base = warp * 32; base < nrows; base += kThreads) {
-            const uint32_t r = base + lane;
-            const int len = r < nrows ? (int)(s_rp[r + 1] - s_rp[r]) : 0;
-            unsigned mask = __ballot_sync(0xffffffffu, len > kMvShortRow);
-            while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const uint32_t rr = base + j;
-                const int lo = (int)(s_rp[rr] - nb), hi = (int)(s_rp[rr + 1] - nb);
-                double s = 0.0;
-                for (int k = lo + lane; k < hi; k += 32) s = dadd(s, s_vals[k]);
-                s = warp_sum(s);
-                if (lane == 0) s_y[rr] = s;
-            }
-        }
-        __syncthreads();
-        for (uint32_t r = tid; r < nrows; r += kThreads) {
-            const uint32_t v = rb + r;
-            const uint32_t d = __ldg(a.deg + v);
-            const double y = epilogue(a, st, v, 0, 1, v, s_y[r], d);
-            my_l1 = dadd(my_l1, y);
-            if (want_dm && d == 0) my_dm = dadd(my_dm, y);
-        }
-    } else {
-        // One long row: every thread sums a fixed strided subset, then a fixed tree.
-        const int64_t lo = a.row_ptr[rb], hi = a.row_ptr[rb + 1];
-        double s = 0.0;
-        constexpr int U = 8;
-        int64_t e = lo + tid;
-        for (; e + (U - 1) * kThreads < hi; e += U * kThreads) {
-            uint32_t u[U];
-            double v[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = ld_stream_u32(a.col + e + j * kThreads);
-#pragma unroll
-            for (int j = 0; j < U; ++j) v[j] = __ldg(a.share_in + u[j]);
-#pragma unroll
-            for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
-        }
-        for (; e < hi; e += kThreads) s = dadd(s, __ldg(a.share_in + ld_stream_u32(a.col + e)));
-        s = block_sum(s, s_red);
-        if (tid == 0) {
-            const uint32_t d = __ldg(a.deg + rb);
-            const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
-            my_l1 = y;
-            if (want_dm && d == 0) my_dm = y;
-        }
-    }
-    const double l1 = block_sum(my_l1, s_red);
-    const double dm = want_dm ? block_sum(my_dm, s_red) : 0.0;
-    if (tid == 0) {
-        s_part[0] = l1;
-        s_part[1] = dm;
-    }
-    __syncthreads();
-    finish_item(a, item, 1, s_part, s_red, s_fin);
-}
-
-// ---------------------------------------------------------------------------
 // K3 (SpMM, B in {8,16,32,64}) lives in cpi_spmm.cuh.  Shape helpers: G =
 // min(B,32) lanes per row, CPL = B/G columns per lane.
 // ---------------------------------------------------------------------------

@@ -14,7 +14,7 @@
 // No Y round trip through HBM, one launch per sweep.
 #pragma once
 
-#include "cpi_spmm4.cuh"
+#include "cpi_frontier.cuh"
 
 namespace tpa {
 

@@ -56,20 +56,9 @@ constexpr size_t kMvDynSmem = mv_dyn_smem<kMvTileNnz, kMvTileRows>();
 struct MvShape {
     int thr, nnz, rows;
 };
-#ifndef TPA_MV_S_THR  // A/B knobs for the small-graph shape (partition.py mirrors the defaults)
-#define TPA_MV_S_THR 128
-#define TPA_MV_S_NNZ 1024
-#define TPA_MV_S_ROWS 256
-#endif
-#ifndef TPA_MV_L_THR  // A/B knobs for the large-graph shape (partition.py mirrors the defaults)
-#define TPA_MV_L_THR 256
-#define TPA_MV_L_NNZ 2048
-#define TPA_MV_L_ROWS 256
-#endif
-constexpr MvShape kMvShapeS{TPA_MV_S_THR, TPA_MV_S_NNZ, TPA_MV_S_ROWS},
-    kMvShapeL{TPA_MV_L_THR, TPA_MV_L_NNZ, TPA_MV_L_ROWS}, kMvShapeW{256, 2048, 512};
+// (partition.py mirrors both shapes and the rule)
+constexpr MvShape kMvShapeS{128, 1024, 256}, kMvShapeL{256, 2048, 256};
 inline MvShape mv_shape(uint64_t n_global) {
-    if (const char* e = std::getenv("TPA_MV_SHAPE")) return e[0] == 'L' ? kMvShapeL : e[0] == 'W' ? kMvShapeW : kMvShapeS;
     return n_global * 8 > (512ull << 20) ? kMvShapeL : kMvShapeS;
 }
 

@@ -29,10 +29,8 @@
 
 #include "cpi_kernels.cuh"
 #include "cpi_spmm.cuh"
-#include "cpi_spmm3.cuh"
-#include "cpi_spmm4.cuh"
 #include "cpi_spmm5.cuh"
-#include "cpi_spmv3.cuh"
+#include "cpi_spmv2.cuh"
 #include "cpi_sweep1.cuh"
 #include "tpa_gpu.h"
 #include "tpa_internal.hpp"
@@ -364,38 +362,10 @@ std::vector<uint2> build_items(const std::vector<int64_t>& rp, uint32_t n, int64
     return items;
 }
 
-// SpMM kernel generation for B = 32 / 64: v4 (lean gather + coalesced
-// epilogue, the measured best) unless TPA_SPMM selects 2 (fused, register
-// pipelined) or 3 (experimental cp.async ring).  B = 8 / 16 always use v2.
-static int spmm_version(int B) {
-    static const int env = [] {
-        const char* e = std::getenv("TPA_SPMM");
-        return e ? std::atoi(e) : 5;
-    }();
-    if (B == 16) return env == 2 ? 2 : 5;  // v5 paired half-warps (TPA_SPMM=2: the v2 kernel)
-    if (B != 32 && B != 64) return 2;
-    return (env >= 2 && env <= 4) ? env : 5;
-}
-
-// v5 rows per block: B = 32 pulls its first sweep (a small frontier: few
-// blocks live) in 16-row blocks and the dense ones in 8-row blocks (half the
-// shared memory per warp: 32 instead of 24 resident warps per SM); B = 64 in
-// 8-row blocks.  TPA_MM5_RB=4/8/16 forces one size (A/B experiments).
-static int mm5_rows(int B, uint32_t step) {
-    static const int env = [] {
-        const char* e = std::getenv("TPA_MM5_RB");
-        const int v = e ? std::atoi(e) : 0;
-        return (v == 4 || v == 8 || v == 16) ? v : 0;
-    }();
-    if (env) return env;
-    static const uint32_t wide_steps = [] {  // A/B: sweeps 1..k in 16-row blocks
-        const char* e = std::getenv("TPA_MM5_WIDE_STEPS");
-        return e ? (uint32_t)std::atoi(e) : 0u;
-    }();
-    if (B == 32) return step <= wide_steps ? 16 : 8;
-    if (B == 16) return 16;  // 2.2 KB of shared memory per warp either way: 1.23 -> 1.13 ms per C2 batch
-    return 8;
-}
+// Rows per block of the fused sweep: B = 16 in 16-row blocks (2.2 KB of shared
+// memory per warp either way: 1.23 -> 1.13 ms per C2 batch), B = 32 / 64 in
+// 8-row blocks (32 resident warps per SM instead of 24).
+static int mm5_rows(int B) { return B == 16 ? 16 : 8; }
 
 template <int B, bool L, int RB>
 static void launch_fused(const Mm4Args& P, int num_sms, cudaStream_t stream) {
@@ -403,9 +373,6 @@ static void launch_fused(const Mm4Args& P, int num_sms, cudaStream_t stream) {
     static const int grid = [num_sms] {
         CK(cudaFuncSetAttribute(k_mm_fused<B, L, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)Sh::kDynSmem));
-        if (const char* e = std::getenv("TPA_MM5_CARVEOUT"))  // A/B: shared memory vs L1 split
-            CK(cudaFuncSetAttribute(k_mm_fused<B, L, RB>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    std::atoi(e)));
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mm_fused<B, L, RB>, Sh::NT, Sh::kDynSmem));
         return std::max(occ, 1) * num_sms;
@@ -423,58 +390,15 @@ static void launch_fused_rb(const Mm4Args& P, int rb, int num_sms, cudaStream_t 
 // Sweeps (of a seed batch) run frontier-driven: push-mark then pull.
 constexpr uint32_t kSparseSweeps = 3;
 
-// SpMV generation: v2 (prefetched tiles, fixed-point residual); TPA_SPMV=1
-// selects v1, TPA_SPMV=3 the warp-independent v3 (measured slower: the B200's
-// L1 sustains ~1 random 8-byte gather/clk/SM, tools/gather8_micro.cu, and v3's
-// per-row shared-memory walk adds to the same pipe).
-static int spmv_version() {
-    static const int env = [] {
-        const char* e = std::getenv("TPA_SPMV");
-        return e ? std::atoi(e) : 2;
-    }();
-    return (env == 1 || env == 3) ? env : 2;
-}
-
-template <int B>
-constexpr size_t mm4_epi_smem() {
-    return (size_t)(Mm4<B>::NT / 32) * 32 * (B + 1) * sizeof(double);
-}
-
-template <int B>
-static void mm4_grids(int num_sms, int& g_gather, int& g_epi) {
-    int o1 = 0, o2 = 0;
-    CK(cudaFuncSetAttribute(k_mm_epi<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mm4_epi_smem<B>()));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_mm_gather<B>, Mm4<B>::NT, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_mm_epi<B>, Mm4<B>::NT, mm4_epi_smem<B>()));
-    g_gather = std::max(1, o1) * num_sms;
-    g_epi = std::max(1, o2) * num_sms;
-}
-
-// Persistent-grid sizing (dynamic smem = ring / row-sum buffers).
+// Persistent-grid sizing of the B = 8 sweep (k_step_spmm2; dynamic smem = row buffers).
 template <int B>
 static int mm_occupancy() {
     int occ = 0;
-    if constexpr (B == 32 || B == 64) {
-        if (spmm_version(B) == 3) {
-            const size_t dyn = Mm3Shape<B>::kDynSmem;
-            CK(cudaFuncSetAttribute(k_step_spmm3<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmm3<B>, Mm3Shape<B>::NT, dyn));
-            return occ;
-        }
-    }
     const size_t dyn = MmShape<B>::kDynSmem;
     CK(cudaFuncSetAttribute(k_step_spmm2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmm2<B>, MmShape<B>::NT, dyn));
     return occ;
 }
-
-// The CSR(Ãᵀ) of the graph with nodes numbered by out-degree (tpa_relabel.cuh).
-struct Relabel {
-    DevBuf row_ptr, col, deg;  // twin CSR(Ãᵀ) and out-degrees, new ids
-    DevBuf perm;               // perm[new id] = old id
-    DevBuf acc;                // window accumulator in new-id order
-    Schedule mv;               // SpMV tiles of the twin
-};
 
 struct Workspace {
     int B = 0;
@@ -482,15 +406,13 @@ struct Workspace {
     // SpMM (B > 1) extras
     DevBuf nz[2], acc_valid, long_cnt, seg_part, work_cnt, fx;
     DevBuf s1_skip, s1_fx;  // the seed push took sweep 1 (cpi_sweep1.cuh); its exact totals
-    int grid = 0;  // persistent grid of k_step_spmm2<B>
-    DevBuf Y, ybits;  // v4: row sums and their written-rows bitmap
+    int grid = 0;  // persistent grid of k_step_spmm2<8>
     DevBuf rowflag, sparse_ctl;  // sparse sweeps: reachable rows; {cost, dense, window count}
     DevBuf wbits, wl;            // sparse sweeps: marked windows (bitmap, list)
     DevBuf big;                  // sparse sweeps: edge chunks of high out-degree frontier rows
     DevBuf limbs;                // partition mode: [3][6] fixed-point limbs (sweep parity 0/1, init) + [6] totals
     DevBuf sl;                   // sparse sweeps: segments of the marked long rows
     DevBuf dm_part;              // caller-supplied x: per-block signed dangling sums
-    int grid_gather = 0, grid_epi = 0;
 };
 
 // Long rows of CSR(Ãᵀ) (in-degree > kLong) cut into kLong-nnz segments, the
@@ -544,7 +466,6 @@ struct tpa_graph {
     DevBuf out_off, out_tgt;  // the out-edge CSR itself (frontier push-marking)
     Schedule mv;  // SpMV work items
     MvShape mv_shape = kMvShapeS;  // SpMV tile shape (mv_shape of the global node count)
-    std::unique_ptr<Relabel> rl;  // relabelled twin for dense-start B = 1 runs (tpa_relabel.cuh), built lazily
     LongRows longs;
     uint32_t n_blocks = 0;  // kMmRows-row blocks
     std::map<int, std::unique_ptr<Workspace>> ws;
@@ -568,14 +489,7 @@ struct tpa_graph {
     uint64_t launches = 0;
     int num_sms = 148;
     std::mutex mu;
-    bool sparse_off = std::getenv("TPA_NO_SPARSE") != nullptr;  // A/B switch
-    bool no_window_list = std::getenv("TPA_NO_WINDOW_LIST") != nullptr;  // A/B switch
-    bool s1_push_off = std::getenv("TPA_NO_SEED_PUSH") != nullptr;       // A/B switch
-    uint64_t sparse_div = [] {  // sparse sweep if the push touches <= m / sparse_div edges
-        const char* e = std::getenv("TPA_SPARSE_DIV");
-        const long v = e ? std::atol(e) : 32;
-        return (uint64_t)(v > 0 ? v : 32);
-    }();
+    static constexpr uint64_t sparse_div = 32;  // sparse sweep if the push touches <= m / 32 edges
     // optional per-sweep-kernel CUDA-event timing (bench instrumentation)
     bool profile = false;
     struct ProfEvent {
@@ -647,27 +561,14 @@ struct tpa_graph {
             CK(cudaMemsetAsync(w.long_cnt.p, 0, w.long_cnt.bytes, stream));
             CK(cudaMemsetAsync(w.work_cnt.p, 0, w.work_cnt.bytes, stream));
             CK(cudaMemsetAsync(w.fx.p, 0, w.fx.bytes, stream));
-            int occ = 0;
-            switch (B) {
-                case 8: occ = mm_occupancy<8>(); break;
-                case 16: occ = mm_occupancy<16>(); break;
-                case 32: occ = mm_occupancy<32>(); break;
-                case 64: occ = mm_occupancy<64>(); break;
-            }
-            w.grid = std::max(1, occ) * num_sms;
-            if (spmm_version(B) >= 4) {
-                if (spmm_version(B) == 4) {  // v4's row sums round-trip HBM (n x B doubles)
-                    w.Y.ensure((size_t)n * B * 8, stream);
-                    w.ybits.ensure(words * 4, stream);
-                }
+            if (B == 8) w.grid = std::max(1, mm_occupancy<8>()) * num_sms;
+            if (B >= 16) {  // the fused sweep's sparse-sweep lists
                 w.rowflag.ensure((size_t)n + 16, stream);
                 w.sparse_ctl.ensure(32, stream);
                 w.big.ensure(mark_chunk_cap(m) * sizeof(ulonglong2), stream);
                 w.sl.ensure(((size_t)longs.n_segs + 1) * 4, stream);
                 w.wbits.ensure(((size_t)n / 4 / 32 + 2) * 4, stream);
                 w.wl.ensure(((size_t)n / 4 + 2) * 4, stream);
-                if (B == 32) mm4_grids<32>(num_sms, w.grid_gather, w.grid_epi);
-                if (B == 64) mm4_grids<64>(num_sms, w.grid_gather, w.grid_epi);
             }
         }
         return w;
@@ -769,17 +670,14 @@ static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
     return std::upper_bound(bounds.begin(), bounds.end(), i) - bounds.begin();
 }
 
-// K2 v2 at one tile shape: dynamic shared memory sized for it (and the
-// TPA_MV_CARVEOUT A/B knob) set once per instantiation.
+// K2 v2 at one tile shape: dynamic shared memory sized for it, set once per
+// instantiation.
 template <bool RF, int THR, int NNZ, int ROWS>
 static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
     constexpr size_t smem = mv_dyn_smem<NNZ, ROWS>();
     static const bool ok = [] {
         CK(cudaFuncSetAttribute(k_step_spmv2<RF, THR, NNZ, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-        if (const char* e = std::getenv("TPA_MV_CARVEOUT"))
-            CK(cudaFuncSetAttribute(k_step_spmv2<RF, THR, NNZ, ROWS>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    std::atoi(e)));
         return true;
     }();
     (void)ok;
@@ -801,21 +699,20 @@ static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
 }
 
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
-                        const SeedList* push_seeds = nullptr, const Schedule* sched = nullptr) {
-    const Schedule& s = sched ? *sched : g->mv;
-    const dim3 grid(B == 1 ? s.n_items : (uint32_t)w.grid), block(kThreads);
+                        const SeedList* push_seeds = nullptr) {
+    const Schedule& s = g->mv;
+    const dim3 grid(B == 1 ? s.n_items : (uint32_t)w.grid);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g->profile) {
         e0 = g->take_event();
         e1 = g->take_event();
         CK(cudaEventRecord(e0, g->stream));
     }
-    const bool v4 = B > 1 && spmm_version(B) >= 4;
-    const int rb = spmm_version(B) == 5 ? mm5_rows(B, a.step) : (B == 64 ? 8 : 16);
-    if (v4) {
-        Mm4Args P{*mm, w.Y.as<double>(), w.ybits.as<uint32_t>(), nullptr, nullptr,
-                  g->longs.blocks_w[LongRows::wi(rb)].as<uint2>(), g->longs.n_blocks_w[LongRows::wi(rb)]};
-        if (spmm_version(B) == 4) CK(cudaMemsetAsync(w.ybits.p, 0, w.ybits.bytes, g->stream));
+    const bool fused = B >= 16;  // B = 8: k_step_spmm2<8>
+    const int rb = mm5_rows(B);
+    if (fused) {
+        Mm4Args P{*mm, nullptr, nullptr, g->longs.blocks_w[LongRows::wi(rb)].as<uint2>(),
+                  g->longs.n_blocks_w[LongRows::wi(rb)]};
         // the first sweeps of a seed batch usually see a small frontier: if it
         // pushes along at most m/32 edges, mark the rows it reaches (push over
         // the out-CSR) and pull only those; the decision is taken on the device
@@ -842,12 +739,12 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             }
             CKL("k_s1_push");
             g->launches += 2;  // k_s1_rows + k_s1_push (the common ++ below is cancelled)
-        } else if (mm->nz_in && a.step <= kSparseSweeps && !g->sparse_off) {
+        } else if (mm->nz_in && a.step <= kSparseSweeps) {
             const uint32_t words = (g->n + 31) / 32;
             auto* ctl = w.sparse_ctl.as<unsigned long long>();
             CK(cudaMemsetAsync(w.sparse_ctl.p, 0, 32, g->stream));
             CK(cudaMemsetAsync(w.rowflag.p, 0, g->n, g->stream));
-            const bool by_win = spmm_version(B) == 5 && !g->no_window_list;
+            const bool by_win = true;
             const int rb_shift = rb == 4 ? 2 : rb == 8 ? 3 : rb == 16 ? 4 : 5;
             if (by_win) CK(cudaMemsetAsync(w.wbits.p, 0, ((size_t)(g->n >> rb_shift) / 32 + 1) * 4, g->stream));
             uint32_t* wl_cnt = reinterpret_cast<uint32_t*>(w.sparse_ctl.as<char>() + 12);
@@ -884,7 +781,7 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
         }
         if (push_seeds) {
             g->launches -= 1;  // no pull this sweep: cancels the common ++ below
-        } else if (spmm_version(B) == 5) {
+        } else {
             const bool last = a.out != nullptr;
             if (B == 16) {
                 if (last) launch_fused_rb<16, true>(P, rb, g->num_sms, g->stream);
@@ -897,33 +794,10 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                 else launch_fused_rb<64, false>(P, rb, g->num_sms, g->stream);
             }
             g->launches -= 1;  // one kernel (the common ++ below counts it)
-        } else if (B == 32) {
-            k_mm_gather<32><<<w.grid_gather, Mm4<32>::NT, 0, g->stream>>>(P);
-            CKL("k_mm_gather<32>");
-            k_mm_epi<32><<<w.grid_epi, Mm4<32>::NT, mm4_epi_smem<32>(), g->stream>>>(P);
-        } else {
-            k_mm_gather<64><<<w.grid_gather, Mm4<64>::NT, 0, g->stream>>>(P);
-            CKL("k_mm_gather<64>");
-            k_mm_epi<64><<<w.grid_epi, Mm4<64>::NT, mm4_epi_smem<64>(), g->stream>>>(P);
         }
         g->launches += 1;  // + the epilogue below
     } else switch (B) {
         case 1:
-            if (spmv_version() == 3 && !g->part) {
-                static const int grid3 = [] {
-                    int occ = 0, dev = 0, sms = 0;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_spmv3, kMv3Threads, 0));
-                    CK(cudaGetDevice(&dev));
-                    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-                    return std::max(occ, 1) * sms;
-                }();
-                const LongRows& L = g->longs;
-                Mv3Args M{a, L.seg_row.as<uint32_t>(), L.seg_lo.as<int64_t>(), L.seg_long.as<uint32_t>(),
-                          L.long_first.as<uint32_t>(), L.long_nseg.as<uint32_t>(), L.n_segs,
-                          L.blocks_w[3].as<uint2>(), L.n_blocks_w[3], w.long_cnt.as<uint32_t>(),
-                          w.seg_part.as<double>(), w.fx.as<unsigned long long>()};
-                k_step_spmv3<<<grid3, kMv3Threads, 0, g->stream>>>(M);
-            } else if (spmv_version() == 2 || g->part)
             {
                 MvArgs M{a, s.item_nnz.as<longlong2>(), w.fx.as<unsigned long long>(),
                          !g->part ? nullptr
@@ -931,45 +805,14 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                                        : w.limbs.as<unsigned long long>() + (a.step & 1) * 6,
                          PeerOut{}, g->part ? g->part->slice : 0u};
                 if (g->part && a.share_out) M.peers = g->peer_out;
-                // the relabelled twin sums its residual row by row (tpa_relabel.cuh)
-                const bool rf = sched && sched != &g->mv;
                 const MvShape& sh = g->mv_shape;
-                if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows) {
-                    if (rf) launch_mv2<true, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
-                    else launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
-                } else if (sh.thr == kMvShapeL.thr && sh.nnz == kMvShapeL.nnz && sh.rows == kMvShapeL.rows) {
-                    if (rf) launch_mv2<true, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
-                    else launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
-                } else {
-                    if (rf) launch_mv2<true, 256, 2048, 512>(M, grid.x, g->stream);
-                    else launch_mv2<false, 256, 2048, 512>(M, grid.x, g->stream);
-                }
-            }
-            else
-            {
-                static const bool smem1 = [] {
-                    CK(cudaFuncSetAttribute(k_step_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kMv1DynSmem));
-                    return true;
-                }();
-                (void)smem1;
-                k_step_spmv<<<grid, block, kMv1DynSmem, g->stream>>>(a);
+                if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows)
+                    launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
+                else
+                    launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
             }
             break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
-        case 16: k_step_spmm2<16><<<grid, MmShape<16>::NT, MmShape<16>::kDynSmem, g->stream>>>(*mm); break;
-        case 32:
-            if (spmm_version(32) == 3)
-                k_step_spmm3<32><<<grid, Mm3Shape<32>::NT, Mm3Shape<32>::kDynSmem, g->stream>>>(*mm);
-            else
-                k_step_spmm2<32><<<grid, MmShape<32>::NT, MmShape<32>::kDynSmem, g->stream>>>(*mm);
-            break;
-        case 64:
-            if (spmm_version(64) == 3)
-                k_step_spmm3<64><<<grid, Mm3Shape<64>::NT, Mm3Shape<64>::kDynSmem, g->stream>>>(*mm);
-            else
-                k_step_spmm2<64><<<grid, MmShape<64>::NT, MmShape<64>::kDynSmem, g->stream>>>(*mm);
-            break;
         default: throw std::invalid_argument("unsupported batch width");
     }
     CKL("k_step (sweep)");
@@ -984,7 +827,6 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
 // per-column state (cpi.cpp:70-81) advances on the device.  Only a run to
 // convergence (terminal < 0) checks the state on the host after the
 // estimated horizon, and continues if a column is still active.
-#include "tpa_relabel.cuh"
 
 static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int B = cfg.B;
@@ -998,35 +840,8 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const double keep = 1.0 - cfg.c;
     ColState* st = w.state.as<ColState>();
     const bool partition = !cfg.bounds.empty() || !cfg.seg_acc.empty();
-    // dense-start B = 1 runs sweep the relabelled twin (tpa_relabel.cuh): the
-    // same additions in the same order, hub shares packed into few lines
-    Relabel* rl = (B == 1 && !partition && !cfg.y_out && !cfg.out && cfg.init == Init::Dense && !cfg.d_x &&
-                   spmv_version() == 2)
-                      ? relabel_view(g)
-                      : nullptr;
-    // A/B (with the twin): TPA_L2_PERSIST_MB of the share vector's hottest
-    // (lowest twin id) entries marked L2-persisting for the sweeps
-    static const size_t rl_persist_env = [] {
-        const char* e = std::getenv("TPA_L2_PERSIST_MB");
-        return e ? (size_t)std::atoi(e) << 20 : (size_t)0;
-    }();
-    const size_t rl_persist = rl ? rl_persist_env : 0;
-    if (rl_persist) {
-        int dev = 0, mx = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev));
-        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)mx, rl_persist)));
-    }
     double* acc_run = cfg.acc;
-    if (rl && cfg.acc) {
-        if (cfg.acc != w.acc.as<double>()) {
-            acc_run = w.acc.as<double>();
-        } else {
-            rl->acc.ensure((size_t)n * 8, g->stream);
-            acc_run = rl->acc.as<double>();
-        }
-    }
-    const uint32_t* const deg_run = rl ? rl->deg.as<uint32_t>() : g->deg.as<uint32_t>();
+    const uint32_t* const deg_run = g->deg.as<uint32_t>();
 
     // accumulator for x⁽⁰⁾, zero the rest
     double* acc0 = nullptr;
@@ -1080,12 +895,11 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     }
 
     StepArgs a{};
-    const Schedule& sch_run = rl ? rl->mv : sch;
-    a.row_ptr = rl ? rl->row_ptr.as<int64_t>() : g->row_ptr.as<int64_t>();
-    a.col = rl ? rl->col.as<uint32_t>() : g->col.as<uint32_t>();
+    a.row_ptr = g->row_ptr.as<int64_t>();
+    a.col = g->col.as<uint32_t>();
     a.deg = deg_run;
-    a.items = sch_run.items.as<uint2>();
-    a.n_items = sch_run.n_items;
+    a.items = sch.items.as<uint2>();
+    a.n_items = sch.n_items;
     a.n = n;
     a.policy = g->policy;
     a.keep = keep;
@@ -1150,17 +964,8 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             // sweep 1 of a seed batch: a push from the seeds (one term per
             // element) instead of a pull over every nonzero
             const bool s1 = mm && i == 1 && cfg.init == Init::Seeds && a.acc && a.share_out && !a.out &&
-                            !cfg.y_out && g->policy != kUniform && spmm_version(B) == 5 && !g->s1_push_off;
-            if (rl && rl_persist) {  // the hub shares (the twin's first ids) persist in L2
-                cudaStreamAttrValue av{};
-                av.accessPolicyWindow.base_ptr = const_cast<double*>(a.share_in);
-                av.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)n * 8, rl_persist);
-                av.accessPolicyWindow.hitRatio = 1.0f;
-                av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-                av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-                CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &av));
-            }
-            launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr, &sch_run);
+                            !cfg.y_out && g->policy != kUniform && B >= 16;
+            launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr);
         }
         done += chunk;
         if ((int64_t)done >= target) break;
@@ -1178,18 +983,6 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             acc_final, mm ? w.acc_valid.as<uint32_t>() : nullptr, n, B, cfg.b_valid, cfg.stranger, cfg.scale,
             cfg.node_major ? 1 : 0, cfg.out);
         CKL("k_combine");
-        ++g->launches;
-    }
-    if (rl_persist) {
-        cudaStreamAttrValue av{};
-        av.accessPolicyWindow.num_bytes = 0;
-        CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &av));
-        CK(cudaCtxResetPersistingL2Cache());
-    }
-    if (rl && cfg.acc) {  // the window accumulator back in original ids
-        k_rl_unpermute<<<grid_for(n, 256, 8 * g->num_sms), 256, 0, g->stream>>>(acc_run, rl->perm.as<uint32_t>(), n,
-                                                                                  cfg.acc);
-        CKL("k_rl_unpermute");
         ++g->launches;
     }
     if (res && cfg.want_state) {
@@ -1454,13 +1247,6 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
             uint64_t thr = UINT64_MAX;
             CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         }
-        if (const char* e = std::getenv("TPA_L2_FETCH")) {  // A/B: L2 fetch granularity for DRAM misses (bytes)
-            CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(e)));
-            size_t v = 0;
-            CK(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
-            if (std::getenv("TPA_DEBUG")) fprintf(stderr, "tpa: L2 fetch granularity %zu\n", v);
-        }
-
         DevBuf d_off, d_tgt, d_src, d_keys;
         d_off.ensure((n + 1ull) * 8, g->stream);
         d_tgt.ensure(m * 4, g->stream);
@@ -1520,7 +1306,6 @@ int tpa_graph_destroy(tpa_graph* g) {
             DeviceGuard dg(g->device);
             // stream-ordered frees first, then drain and drop the stream
             g->ws.clear();
-            g->rl.reset();
             g->row_ptr.release();
             g->col.release();
             g->deg.release();
@@ -1596,7 +1381,6 @@ int tpa_graph_info(const tpa_graph* g, uint32_t* n, uint64_t* m, uint64_t* finge
         if (device_bytes) {
             uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->longs.seg_lo.bytes * 2 +
                          g->out_off.bytes + g->out_tgt.bytes;
-            if (g->rl) b += g->rl->row_ptr.bytes + g->rl->col.bytes + g->rl->deg.bytes + g->rl->perm.bytes + g->rl->acc.bytes;
             for (auto& kv : g->ws) {
                 const Workspace& w = *kv.second;
                 b += w.share[0].bytes + w.share[1].bytes + w.acc.bytes + w.part.bytes + w.gpart.bytes;

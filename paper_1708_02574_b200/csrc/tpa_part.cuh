@@ -390,8 +390,7 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
             const bool last = (int64_t)i == target;
             const bool inw = i >= cfg.start && (cfg.terminal < 0 || (int64_t)i <= cfg.terminal);
             // in-process groups: each sweep stores its shares into the peers' buffers
-            const bool fused = Pg.size() > 1 && Pg.size() <= (size_t)kMaxPeerOut + 1 && !last &&
-                               !std::getenv("TPA_GROUP_COPY");
+            const bool fused = Pg.size() > 1 && Pg.size() <= (size_t)kMaxPeerOut + 1 && !last;
             for (size_t k = 0; k < Pg.size(); ++k) {
                 tpa_graph* g = Pg[k];
                 DeviceGuard dg(g->device);

@@ -14,7 +14,6 @@ Queries (independent seeds) run on whole-graph replicas (``DeviceGraph``).
 """
 from __future__ import annotations
 
-import os
 
 import ctypes as C
 from typing import Optional, Sequence
@@ -30,14 +29,11 @@ COMM_ID_BYTES = 128
 
 # SpMV tiling constants (csrc/cpi_kernels.cuh kMvTileNnz / kMvTileRows)
 TILE_NNZ, TILE_ROWS = 2048, 512  # the largest tile shape (bounds; tests)
-SHAPES = {"S": (1024, 256), "L": (2048, 256), "W": (2048, 512)}  # (nnz, rows), cpi_spmv2.cuh
+SHAPES = {"S": (1024, 256), "L": (2048, 256)}  # (nnz, rows), cpi_spmv2.cuh
 
 
 def tile_shape(n: int) -> tuple:
     """(nnz, rows) per SpMV tile for a graph of n nodes (cpi_spmv2.cuh mv_shape)."""
-    e = os.environ.get("TPA_MV_SHAPE")
-    if e:
-        return SHAPES["L"] if e[0] == "L" else SHAPES["W"] if e[0] == "W" else SHAPES["S"]
     return SHAPES["L"] if n * 8 > (512 << 20) else SHAPES["S"]
 
 
