@@ -19,9 +19,11 @@ roofline fraction of the dominant sweep kernel reported beside it.
 oracle port if that is absent) on the host cores, same config and metric.
 
 Multi-GPU (torchrun, one rank per GPU): the one job strong-scaled --
-PageRank preprocessing row-partitioned across the ranks (one NCCL all-gather of
-the iterate's shares + exact residual limbs per sweep) and the job's queries
-split over the ranks' whole-graph replicas (no data-path collective);
+PageRank preprocessing row-partitioned across the ranks (the fused exchange:
+each sweep's epilogue stores the iterate's shares + exact residual limbs
+straight into every peer's buffer over NVLink, CUDA IPC; TPA_BENCH_TRANSPORT=nccl
+for one NCCL all-gather per sweep instead) and the job's queries split over the
+ranks' whole-graph replicas (no data-path collective);
 TPA_BENCH_REPLICAS=1 runs N independent jobs instead (weak scaling).
 
 Configs (--config): c1..c5 of BASELINE.json; c4/c5 graphs are generated and
@@ -425,7 +427,11 @@ def run_ours(args):
     pg = None
     if partitioned:
         if world > 1:
-            pg = P.PartitionedGraph.from_process_group(g, device=local)
+            # the fused exchange (every sweep stores its shares into the peers'
+            # buffers over NVLink, CUDA IPC); TPA_BENCH_TRANSPORT=nccl: one
+            # NCCL all-gather per sweep instead
+            pg = P.PartitionedGraph.from_process_group(
+                g, device=local, transport=os.environ.get("TPA_BENCH_TRANSPORT", "ipc"))
         else:
             pg = P.PartitionedGraph(g, 1, 0, comm_id=P.partition.comm_unique_id(), device=local)
         N.check(lib.tpa_graph_set_stream(pg.h, stream.cuda_stream))
@@ -705,8 +711,8 @@ def run_ours(args):
                         "device top-10 per seed kept resident (tpa_query_batch_topk)" if resident_topk else
                         "the B full score vectors of every batch written to a resident [B][n] buffer"),
             "device_mem_gb": torch.cuda.max_memory_reserved(dev) / 1e9 + dg.device_bytes() / 1e9,
-            "parallelism": (f"row-partitioned preprocess (one NCCL all-gather per sweep: shares + exact residual limbs) + "
-                            f"queries split over {world} whole-graph replicas" if partitioned else
+            "parallelism": (f"row-partitioned preprocess ({pg.transport} exchange per sweep: shares + exact residual "
+                            f"limbs) + queries split over {world} whole-graph replicas" if partitioned else
                             f"independent replicas x{world}" if world > 1 else "single GPU"),
         }
         print(json.dumps(line), flush=True)

@@ -212,6 +212,22 @@ int tpa_comm_unique_id(void *id_out /* TPA_COMM_ID_BYTES */);
 int tpa_graph_create_part(uint32_t n, uint64_t m, const uint64_t *out_offsets,
                           const uint32_t *out_targets, int policy, uint64_t fingerprint, int device,
                           uint32_t nranks, uint32_t rank, const void *comm_id, tpa_graph **out);
+/* One process per GPU over CUDA IPC: the fused exchange.  Each rank's SpMV
+ * epilogue stores its shares (and its exact residual limbs) straight into
+ * every peer's share buffer -- over NVLink between GPUs -- so the exchange
+ * overlaps the sweep instead of following it as a collective.  Two steps:
+ * create (every rank; fills its TPA_IPC_BLOB_BYTES export blob), exchange the
+ * blobs out of band (e.g. torch.distributed all_gather_object), then attach
+ * with all nranks blobs in rank order.  Ranks may share a device (the stream
+ * waits are interprocess events, no kernel waits on another).  Calls as for
+ * tpa_graph_create_part; 1..16 ranks.  Same results as one GPU, bit for bit. */
+#define TPA_IPC_BLOB_BYTES 1024
+int tpa_graph_create_part_ipc(uint32_t n, uint64_t m, const uint64_t *out_offsets,
+                              const uint32_t *out_targets, int policy, uint64_t fingerprint,
+                              int device, uint32_t nranks, uint32_t rank, void *blob_out,
+                              tpa_graph **out);
+int tpa_part_ipc_attach(tpa_graph *g, const void *blobs /* nranks x TPA_IPC_BLOB_BYTES */);
+
 /* Partition geometry: rows [row_begin, row_end) of `nranks`; `slice` = padded
  * rows per partition in the share layout. */
 int tpa_graph_part_info(const tpa_graph *g, uint32_t *nranks, uint32_t *rank, uint32_t *row_begin,

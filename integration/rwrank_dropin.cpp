@@ -10,12 +10,13 @@
 // recipe.  The reference's `threads` arguments select host threads there and
 // are accepted and ignored here.
 #include <algorithm>
+#include <cstring>
 #include <memory>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
-#include <unordered_map>
+#include <vector>
 
 #include "rwrank/cpi.hpp"
 #include "rwrank/graph.hpp"
@@ -24,18 +25,96 @@
 
 namespace {
 
-// One device-resident CSR(A^T) per host Graph, rebuilt if the Graph at that
+// Device-resident CSR(A^T) per host Graph, rebuilt if the Graph at that
 // address changed (its fingerprint covers n, m, offsets, targets, policy).
+// At most kGraphCache graphs stay resident (least recently used evicted; a
+// caller still holding the shared_ptr keeps its handle alive).
+constexpr size_t kGraphCache = 4;
+struct GraphSlot {
+    const rwrank::Graph* key;
+    std::shared_ptr<rwrank_gpu::DeviceGraph> dg;
+};
+std::mutex g_mu;
+// Deliberately never destroyed: device handles must not be released from
+// static destructors, which may run after the CUDA runtime has shut down.
+auto* g_graphs = new std::vector<GraphSlot>();  // most recent last
+
 std::shared_ptr<rwrank_gpu::DeviceGraph> device_graph(const rwrank::Graph& g) {
-    static std::mutex mu;
-    // Deliberately never destroyed: device handles must not be released from
-    // static destructors, which may run after the CUDA runtime has shut down.
-    static auto* cache = new std::unordered_map<const rwrank::Graph*, std::shared_ptr<rwrank_gpu::DeviceGraph>>();
-    std::lock_guard<std::mutex> lk(mu);
-    auto& slot = (*cache)[&g];
-    if (!slot || slot->fingerprint() != g.fingerprint() || slot->node_count() != g.node_count())
-        slot = std::make_shared<rwrank_gpu::DeviceGraph>(g);
-    return slot;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& v = *g_graphs;
+    for (size_t i = 0; i < v.size(); ++i) {
+        if (v[i].key != &g) continue;
+        GraphSlot s = std::move(v[i]);
+        v.erase(v.begin() + i);
+        if (s.dg->fingerprint() != g.fingerprint() || s.dg->node_count() != g.node_count()) break;
+        v.push_back(std::move(s));
+        return v.back().dg;
+    }
+    if (v.size() >= kGraphCache) v.erase(v.begin());
+    v.push_back({&g, std::make_shared<rwrank_gpu::DeviceGraph>(g)});
+    return v.back().dg;
+}
+
+// Device copies of stranger vectors, so query() does not upload n doubles per
+// call (and concurrent queries on one artifact share one copy).  Keyed by the
+// device graph, the vector's buffer and size and the artifact's scalars, and
+// checked against 64 strided entries of the vector captured at upload: an
+// in-place rewrite of the scores is caught unless it leaves every sampled
+// entry bit-identical.  At most kArtifactCache entries (LRU).
+constexpr size_t kArtifactCache = 8, kSample = 64;
+struct ArtSlot {
+    const rwrank_gpu::DeviceGraph* g;
+    const double* data;
+    size_t n;
+    uint64_t fp;
+    double c, eps;
+    uint32_t T;
+    std::vector<double> sample;
+    std::shared_ptr<rwrank_gpu::DeviceGraph> keep_g;
+    std::shared_ptr<rwrank_gpu::DeviceArtifact> a;
+};
+auto* g_arts = new std::vector<ArtSlot>();
+
+std::vector<double> sample_of(const std::vector<double>& v) {
+    std::vector<double> s;
+    if (v.empty()) return s;
+    s.reserve(kSample);
+    for (size_t j = 0; j < kSample; ++j) s.push_back(v[j * (v.size() - 1) / (kSample - 1)]);
+    return s;
+}
+
+bool same_bits(const std::vector<double>& a, const std::vector<double>& b) {
+    return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), a.size() * 8) == 0);
+}
+
+std::shared_ptr<rwrank_gpu::DeviceArtifact> device_artifact(const std::shared_ptr<rwrank_gpu::DeviceGraph>& dg,
+                                                            const rwrank::StrangerArtifact& art,
+                                                            std::unique_ptr<rwrank_gpu::DeviceArtifact> fresh = nullptr) {
+    const auto& v = art.stranger_scores;
+    std::vector<double> smp = sample_of(v);
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& c = *g_arts;
+    for (size_t i = 0; i < c.size(); ++i) {
+        ArtSlot& e = c[i];
+        if (e.g == dg.get() && e.data == v.data() && e.n == v.size() && e.fp == art.graph_fingerprint &&
+            e.c == art.restart_prob && e.eps == art.tolerance && e.T == art.stranger_start) {
+            ArtSlot s = std::move(e);
+            c.erase(c.begin() + i);
+            if (!fresh && same_bits(s.sample, smp)) {
+                c.push_back(std::move(s));
+                return c.back().a;
+            }
+            break;  // stale (rewritten in place) or replaced: upload anew
+        }
+    }
+    if (c.size() >= kArtifactCache) c.erase(c.begin());
+    std::shared_ptr<rwrank_gpu::DeviceArtifact> a =
+        fresh ? std::shared_ptr<rwrank_gpu::DeviceArtifact>(std::move(fresh))
+              : std::make_shared<rwrank_gpu::DeviceArtifact>(*dg, v, art.graph_fingerprint, art.restart_prob,
+                                                             art.tolerance, art.stranger_start);
+    c.push_back({dg.get(), v.data(), v.size(), art.graph_fingerprint, art.restart_prob, art.tolerance,
+                 art.stranger_start, std::move(smp), dg, a});
+    return a;
 }
 
 bool is_all_nodes(const rwrank::SeedSet& s, rwrank::NodeId n) {
@@ -137,11 +216,15 @@ std::vector<ScoreVector> cpi_partition(const Graph& g, const SeedSet& seeds, dou
 StrangerArtifact preprocess(const Graph& g, double c, double eps, std::uint32_t stranger_start, int) {
     auto dg = device_graph(g);
     StrangerArtifact a;
-    a.stranger_scores = rwrank_gpu::preprocess(*dg, c, eps, stranger_start);
+    std::unique_ptr<rwrank_gpu::DeviceArtifact> keep;
+    a.stranger_scores = rwrank_gpu::preprocess(*dg, c, eps, stranger_start, &keep);
     a.graph_fingerprint = g.fingerprint();
     a.restart_prob = c;
     a.tolerance = eps;
     a.stranger_start = stranger_start;
+    // the vector's buffer survives the moves into the caller's artifact: its
+    // queries find this device copy instead of uploading the scores again
+    device_artifact(dg, a, std::move(keep));
     return a;
 }
 
@@ -156,9 +239,8 @@ ScoreVector query(const Graph& g, const StrangerArtifact& artifact, NodeId seed,
     if (family_end < 1 || family_end >= artifact.stranger_start)
         throw std::invalid_argument("family_end (S) must satisfy 1 <= S < T");
     auto dg = device_graph(g);
-    rwrank_gpu::DeviceArtifact da(*dg, artifact.stranger_scores, artifact.graph_fingerprint, artifact.restart_prob,
-                                  artifact.tolerance, artifact.stranger_start);
-    return rwrank_gpu::query(*dg, da, seed, family_end);
+    auto da = device_artifact(dg, artifact);
+    return rwrank_gpu::query(*dg, *da, seed, family_end);
 }
 
 ScoreVector query_na(const Graph& g, NodeId seed, const TpaParams& params, int) {

@@ -61,6 +61,9 @@ SIGNATURES = {
     "tpa_query_batch_topk": ([_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _int], _int),
     "tpa_comm_unique_id": ([_vp], _int),
     "tpa_graph_create_part": ([_u32, _u64, _vp, _vp, _int, _u64, _int, _u32, _u32, _vp, C.POINTER(_vp)], _int),
+    "tpa_graph_create_part_ipc": ([_u32, _u64, _vp, _vp, _int, _u64, _int, _u32, _u32, _vp, C.POINTER(_vp)],
+                                  _int),
+    "tpa_part_ipc_attach": ([_vp, _vp], _int),
     "tpa_graph_part_info": ([_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32),
                              C.POINTER(_u32)], _int),
     "tpa_group_create": ([_u32, _u64, _vp, _vp, _int, _u64, _vp, _u32, C.POINTER(_vp)], _int),

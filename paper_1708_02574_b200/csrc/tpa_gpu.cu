@@ -78,14 +78,38 @@ struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
     const cudaStream_t* sp = nullptr;
+    bool plain = false;  // cudaMalloc'd (exportable by CUDA IPC), freed by cudaFree
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFreeAsync(p, *sp);
+        if (p) {
+            if (plain) {
+                cudaStreamSynchronize(*sp);
+                cudaFree(p);
+            } else {
+                cudaFreeAsync(p, *sp);
+            }
+        }
         p = nullptr;
         bytes = 0;
+        plain = false;
+    }
+    // A buffer another process can map (cudaIpcGetMemHandle needs a cudaMalloc base).
+    void ensure_plain(size_t nbytes, const cudaStream_t& stream) {
+        if (bytes >= nbytes && p && plain) return;
+        release();
+        const size_t want = nbytes ? nbytes : 16;
+        if (cudaMalloc(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            throw alloc_error("cudaMalloc of " + std::to_string(want) + " bytes failed");
+        }
+        CK(cudaMemsetAsync(p, 0, want, stream));
+        sp = &stream;
+        bytes = want;
+        plain = true;
     }
     void ensure(size_t nbytes, const cudaStream_t& stream) {
         if (bytes >= nbytes && p) return;
@@ -107,6 +131,7 @@ struct DevBuf {
         std::swap(p, o.p);
         std::swap(bytes, o.bytes);
         std::swap(sp, o.sp);
+        std::swap(plain, o.plain);
     }
 };
 
@@ -438,6 +463,29 @@ struct LongRows {
 // moves the shares and the totals together.
 constexpr uint32_t kLimbPad = 8;
 
+// One process per GPU over CUDA IPC (tpa_part.cuh): every rank maps its
+// peers' share ping-pong buffers and limb slots and stores its shares into
+// them from the sweep epilogue (the exchange IS the sweep's stores); per
+// exchange point each rank records an interprocess event and the ranks meet
+// on a host-side stage counter in POSIX shared memory, so each stream waits
+// on exactly the peers' matching records (no kernel ever waits on a kernel).
+constexpr int kIpcRing = 4;
+struct IpcState {
+    struct Peer {
+        double* share[2] = {nullptr, nullptr};
+        unsigned long long* limbs = nullptr;
+        cudaEvent_t ev[kIpcRing] = {};
+    };
+    std::vector<Peer> peers;  // nranks; the own entry holds local pointers
+    cudaEvent_t own_ev[kIpcRing] = {};
+    uint64_t stage = 0;       // exchange points passed (the same sequence on every rank)
+    char shm_name[64] = {0};
+    volatile uint64_t* shm = nullptr;  // nranks stage counters, 64 bytes apart
+    size_t shm_bytes = 0;
+    bool shm_owner = false;
+    bool attached = false;
+};
+
 struct PartInfo {
     uint32_t nranks = 1, rank = 0;
     uint32_t n_global = 0;
@@ -446,6 +494,7 @@ struct PartInfo {
     uint32_t slice = 0;            // S: rows of the largest partition
     uint32_t stride = 0;           // S + kLimbPad: a partition's span in the share layout
     ncclComm_t comm = nullptr;     // one rank per process; null: in-process group or nranks = 1
+    std::unique_ptr<IpcState> ipc;  // one rank per process over CUDA IPC (tpa_part.cuh)
     uint32_t row_begin() const { return bounds[rank]; }
     uint32_t rows(uint32_t r) const { return bounds[r + 1] - bounds[r]; }
 };
@@ -1105,12 +1154,13 @@ static void run_seed_batch(tpa_graph* g, const uint32_t* seeds, uint32_t Btot, d
 namespace tpa {
 static void require_whole(const tpa_graph* g, const char* what);
 static void part_comm_destroy(ncclComm_t c);
+static void ipc_teardown(tpa_graph* g);
 static void part_cpi_run(std::vector<tpa_graph*>& Pg, const uint32_t* seeds, uint64_t n_seeds, double c,
                          double eps, uint32_t start_iter, int64_t terminal_iter, double* out_scores,
                          uint32_t* iterations_run, int* converged, double* residual_l1);
 static void part_preprocess(std::vector<tpa_graph*>& Pg, double c, double eps, uint32_t T, double* out);
 static void require_solo_part(const tpa_graph* g) {
-    if (g->part->nranks > 1 && !g->part->comm)
+    if (g->part->nranks > 1 && !g->part->comm && !g->part->ipc)
         throw std::invalid_argument("a group partition runs through the tpa_group_* calls");
 }
 }  // namespace tpa
@@ -1255,8 +1305,14 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         g->col.ensure(m * 4, g->stream);
         g->deg.ensure((size_t)n * 4, g->stream);
         g->row_ptr.ensure((n + 1ull) * 8, g->stream);
+        // one upload per array: the out-edge CSR stays on the device (frontier
+        // push-marking of sparse sweeps) and the sort keys are a device copy
+        g->out_tgt.ensure(std::max<uint64_t>(m, 1) * 4, g->stream);
         CK(cudaMemcpyAsync(d_off.p, out_offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
-        if (m) CK(cudaMemcpyAsync(d_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
+        if (m) {
+            CK(cudaMemcpyAsync(g->out_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(d_tgt.p, g->out_tgt.p, m * 4, cudaMemcpyDeviceToDevice, s));
+        }
         const int blocks = 8 * g->num_sms;
         k_degrees<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>(), n, g->deg.as<uint32_t>());
         k_expand_src<<<blocks, 256, 0, s>>>(d_off.as<uint64_t>(), n, d_src.as<uint32_t>());
@@ -1279,14 +1335,9 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         d_src.release();
         d_tgt.release();
         k_row_ptr<<<blocks, 256, 0, s>>>(d_keys.as<uint32_t>(), m, n, g->row_ptr.as<int64_t>());
-        // keep the out-edge CSR (frontier push-marking of sparse sweeps)
-        g->out_off.ensure((n + 1ull) * 8, g->stream);
-        g->out_tgt.ensure(std::max<uint64_t>(m, 1) * 4, g->stream);
-        CK(cudaMemcpyAsync(g->out_off.p, out_offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, s));
-        if (m) CK(cudaMemcpyAsync(g->out_tgt.p, out_targets, m * 4, cudaMemcpyHostToDevice, s));
+        g->out_off.swap(d_off);  // the uploaded offsets are the out-CSR's
         CKL("k_row_ptr");
         d_keys.release();
-        d_off.release();
         std::vector<int64_t> rp(n + 1ull);
         CK(cudaMemcpyAsync(rp.data(), g->row_ptr.p, (n + 1ull) * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1304,6 +1355,7 @@ int tpa_graph_destroy(tpa_graph* g) {
         if (g_exiting) return;  // process exit: the CUDA runtime may already be gone
         {
             DeviceGuard dg(g->device);
+            if (g->part && g->part->ipc) ipc_teardown(g);  // peers' mappings before our buffers
             // stream-ordered frees first, then drain and drop the stream
             g->ws.clear();
             g->row_ptr.release();

@@ -11,15 +11,28 @@
 //   * each partition's limbs ride at the end of its span of the share buffer,
 //     so ONE in-place all-gather per sweep moves shares and totals (a sweep
 //     without a next iterate -- the terminal one -- all-reduces the limbs).
-// Two transports with one driver (run_cpi_part):
-//   * one process per GPU: NCCL (in-place ncclAllGather of the span) on the
-//     partition's stream;
+// Three transports with one driver (run_cpi_part):
+//   * one process per GPU over CUDA IPC -- the fused exchange: each rank maps
+//     its peers' share buffers and the sweep epilogue stores every share (and
+//     the tile limbs) straight into them, so the exchange rides on the
+//     sweep's own stores (over NVLink between GPUs) instead of a collective
+//     after it; ranks meet per sweep on interprocess events ordered by a
+//     host-side stage counter (IpcState);
+//   * one process per GPU over NCCL (in-place ncclAllGather of the span) on
+//     the partition's stream;
 //   * one process driving all partitions (tpa_group): stream-ordered peer
 //     copies (cudaMemcpyPeerAsync) and a limb-sum kernel, no host sync.
 // Included at the end of tpa_gpu.cu.
 #pragma once
 
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <chrono>
 
 namespace tpa {
 
@@ -240,6 +253,68 @@ static unsigned long long* limbs_at(tpa_graph* g, int slot, int share) {
     return reinterpret_cast<unsigned long long*>(w.share[share].as<double>() + (size_t)P.rank * P.stride + P.slice);
 }
 
+// ---- CUDA IPC transport ------------------------------------------------------
+struct IpcBlob {
+    uint64_t magic;
+    uint32_t nranks, rank;
+    cudaIpcMemHandle_t share[2], limbs;
+    cudaIpcEventHandle_t ev[kIpcRing];
+    char shm_name[64];
+};
+constexpr uint64_t kIpcMagic = 0x3130435049415054ull;  // "TPAIPC01"
+static_assert(sizeof(IpcBlob) <= TPA_IPC_BLOB_BYTES, "IPC blob size");
+
+static uint64_t* ipc_counter(IpcState& I, uint32_t r) { return const_cast<uint64_t*>(I.shm + (size_t)r * 8); }
+
+// One exchange point: record this rank's event for the stage, publish the
+// stage, wait (host) until every peer has published it -- i.e. enqueued its
+// own record -- and make the stream wait on the peers' records.  A rank can
+// re-record a ring slot only after every peer has passed the previous stage,
+// so each wait refers to the matching record.
+static void ipc_exchange(tpa_graph* g) {
+    IpcState& I = *g->part->ipc;
+    const PartInfo& P = *g->part;
+    if (!I.attached) throw std::logic_error("IPC partition used before tpa_part_ipc_attach");
+    const uint64_t st = ++I.stage;
+    const int slot = (int)(st % kIpcRing);
+    CK(cudaEventRecord(I.own_ev[slot], g->stream));
+    __atomic_store_n(ipc_counter(I, P.rank), st, __ATOMIC_RELEASE);
+    for (uint32_t r = 0; r < P.nranks; ++r) {
+        if (r == P.rank) continue;
+        uint64_t* c = ipc_counter(I, r);
+        uint64_t spins = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (__atomic_load_n(c, __ATOMIC_ACQUIRE) < st) {
+            if (++spins < 4096) continue;
+            sched_yield();
+            if ((spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(600))
+                throw std::runtime_error("IPC partition: rank " + std::to_string(r) + " never reached exchange " +
+                                         std::to_string(st));
+        }
+        CK(cudaStreamWaitEvent(g->stream, I.peers[r].ev[slot], 0));
+    }
+}
+
+static void ipc_teardown(tpa_graph* g) {
+    IpcState& I = *g->part->ipc;
+    cudaStreamSynchronize(g->stream);
+    for (uint32_t r = 0; r < I.peers.size(); ++r) {
+        if (r == g->part->rank) continue;
+        IpcState::Peer& q = I.peers[r];
+        for (double* p : q.share)
+            if (p) cudaIpcCloseMemHandle(p);
+        if (q.limbs) cudaIpcCloseMemHandle(q.limbs);
+        for (cudaEvent_t e : q.ev)
+            if (e) cudaEventDestroy(e);
+    }
+    for (cudaEvent_t e : I.own_ev)
+        if (e) cudaEventDestroy(e);
+    if (I.shm) munmap(const_cast<uint64_t*>(I.shm), I.shm_bytes);
+    if (I.shm_owner) shm_unlink(I.shm_name);
+    g->part->ipc.reset();
+    cudaGetLastError();
+}
+
 // Every partition's totals for `slot`: with a share buffer, one in-place
 // all-gather of the spans (shares + limbs) and a local sum of the G limb
 // sets; without, an all-reduce of the limbs.  Stream-ordered, no host sync.
@@ -256,6 +331,30 @@ static void part_exchange(std::vector<tpa_graph*>& Pg, int slot, int share, bool
         CKL("k_sum_limbs");
         ++g->launches;
     };
+    if (Pg.size() == 1 && Pg[0]->part->ipc) {
+        tpa_graph* g = Pg[0];
+        Workspace& w = g->workspace(1);
+        PartInfo& P = *g->part;
+        IpcState& I = *P.ipc;
+        if (share >= 0) {
+            if (!stored)  // x⁰: this rank's span (shares + limbs) into every peer's buffer
+                for (uint32_t r = 0; r < G; ++r)
+                    if (r != P.rank)
+                        CK(cudaMemcpyAsync(I.peers[r].share[share] + (size_t)P.rank * P.stride,
+                                           w.share[share].as<double>() + (size_t)P.rank * P.stride,
+                                           (size_t)P.stride * 8, cudaMemcpyDeviceToDevice, g->stream));
+            ipc_exchange(g);
+            sum_local(g);
+        } else {
+            ipc_exchange(g);
+            LimbPtrs lp{};
+            for (uint32_t r = 0; r < G; ++r) lp.p[r] = I.peers[r].limbs + slot * 6;
+            k_sum_limbs<<<1, 32, 0, g->stream>>>(lp, G, limbs_total(w));
+            CKL("k_sum_limbs");
+            ++g->launches;
+        }
+        return;
+    }
     if (Pg.size() == 1) {
         tpa_graph* g = Pg[0];
         Workspace& w = g->workspace(1);
@@ -316,6 +415,11 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
     const int active0 = cfg.terminal != 0;
     std::vector<DevBuf> dx(Pg.size());
     std::vector<StepArgs> A(Pg.size());
+    const bool ipc = Pg.size() == 1 && Pg[0]->part->ipc != nullptr;
+    if (ipc) {  // every rank is done with the previous run's buffers before any peer store
+        DeviceGuard dg(Pg[0]->device);
+        ipc_exchange(Pg[0]);
+    }
     // x⁰ (cpi.cpp:59-63), accumulated iff the window starts at 0
     for (size_t k = 0; k < Pg.size(); ++k) {
         tpa_graph* g = Pg[k];
@@ -390,7 +494,8 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
             const bool last = (int64_t)i == target;
             const bool inw = i >= cfg.start && (cfg.terminal < 0 || (int64_t)i <= cfg.terminal);
             // in-process groups: each sweep stores its shares into the peers' buffers
-            const bool fused = Pg.size() > 1 && Pg.size() <= (size_t)kMaxPeerOut + 1 && !last;
+            const bool fused = (ipc ? G <= (uint32_t)kMaxPeerOut + 1
+                                    : Pg.size() > 1 && Pg.size() <= (size_t)kMaxPeerOut + 1) && !last;
             for (size_t k = 0; k < Pg.size(); ++k) {
                 tpa_graph* g = Pg[k];
                 DeviceGuard dg(g->device);
@@ -398,7 +503,11 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
                 const PartInfo& P = *g->part;
                 StepArgs& a = A[k];
                 g->peer_out = PeerOut{};
-                if (fused)
+                if (fused && ipc)
+                    for (uint32_t q = 0; q < G; ++q)
+                        if (q != P.rank)
+                            g->peer_out.p[g->peer_out.n++] = P.ipc->peers[q].share[i & 1] + (size_t)P.rank * P.stride;
+                if (fused && !ipc)
                     for (size_t q = 0; q < Pg.size(); ++q)
                         if (q != k)
                             g->peer_out.p[g->peer_out.n++] =
@@ -447,7 +556,21 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
         DeviceGuard dg(g->device);
         Workspace& w = g->workspace(1);
         const PartInfo& P = *g->part;
-        if (Pg.size() == 1 && P.comm) {
+        if (ipc) {
+            // the accumulators through the share buffers: each rank stores its
+            // rows into every rank's buffer, then reads all spans
+            IpcState& I = *P.ipc;
+            ipc_exchange(g);  // every rank past its last sweep
+            for (uint32_t r = 0; r < G; ++r)
+                if (g->n)
+                    CK(cudaMemcpyAsync(I.peers[r].share[0] + (size_t)P.rank * P.stride, w.acc.p, (size_t)g->n * 8,
+                                       cudaMemcpyDeviceToDevice, g->stream));
+            ipc_exchange(g);
+            for (uint32_t r = 0; r < G; ++r)
+                if (P.rows(r))
+                    CK(cudaMemcpyAsync(cfg.out + P.bounds[r], w.share[0].as<double>() + (size_t)r * P.stride,
+                                       (size_t)P.rows(r) * 8, cudaMemcpyDefault, g->stream));
+        } else if (Pg.size() == 1 && P.comm) {
             DevBuf pad;
             pad.ensure((size_t)G * P.slice * 8, g->stream);
             if (g->n)
@@ -581,6 +704,111 @@ int tpa_graph_create_part(uint32_t n, uint64_t m, const uint64_t* out_offsets, c
             NCK(nccl().CommInitRank(&g->part->comm, (int)nranks, id, (int)rank));
         }
         *out = g.release();
+    });
+}
+
+int tpa_graph_create_part_ipc(uint32_t n, uint64_t m, const uint64_t* out_offsets, const uint32_t* out_targets,
+                              int policy, uint64_t fingerprint, int device, uint32_t nranks, uint32_t rank,
+                              void* blob_out, tpa_graph** out) {
+    return guard([&] {
+        if (!out || !blob_out) throw std::invalid_argument("null output");
+        if (nranks - 1 > (uint32_t)kMaxPeerOut) throw std::invalid_argument("an IPC partition has 1..16 ranks");
+        std::unique_ptr<tpa_graph, int (*)(tpa_graph*)> g(
+            make_part_graph(n, m, out_offsets, out_targets, policy, fingerprint, device, nranks, rank),
+            tpa_graph_destroy);
+        DeviceGuard dg(device);
+        PartInfo& P = *g->part;
+        P.ipc = std::make_unique<IpcState>();
+        IpcState& I = *P.ipc;
+        I.peers.resize(nranks);
+        // the exported buffers (cudaMalloc): the share ping-pong in the padded
+        // global layout and the limb slots; workspace(1) keeps them
+        auto w = std::make_unique<Workspace>();
+        w->B = 1;
+        const size_t nbs = (size_t)nranks * P.stride * sizeof(double);
+        w->share[0].ensure_plain(nbs, g->stream);
+        w->share[1].ensure_plain(nbs, g->stream);
+        w->limbs.ensure_plain(24 * 8, g->stream);
+        g->ws[1] = std::move(w);
+        Workspace& ws = g->workspace(1);
+        IpcBlob b{};
+        b.magic = kIpcMagic;
+        b.nranks = nranks;
+        b.rank = rank;
+        for (int k = 0; k < 2; ++k) CK(cudaIpcGetMemHandle(&b.share[k], ws.share[k].p));
+        CK(cudaIpcGetMemHandle(&b.limbs, ws.limbs.p));
+        for (int k = 0; k < kIpcRing; ++k) {
+            CK(cudaEventCreateWithFlags(&I.own_ev[k], cudaEventDisableTiming | cudaEventInterprocess));
+            CK(cudaIpcGetEventHandle(&b.ev[k], I.own_ev[k]));
+        }
+        IpcState::Peer& me = I.peers[rank];
+        me.share[0] = ws.share[0].as<double>();
+        me.share[1] = ws.share[1].as<double>();
+        me.limbs = ws.limbs.as<unsigned long long>();
+        for (int k = 0; k < kIpcRing; ++k) me.ev[k] = I.own_ev[k];
+        I.shm_bytes = (size_t)nranks * 64;
+        if (rank == 0) {  // the stage counters: created by rank 0, opened by the others at attach
+            static std::atomic<uint64_t> seq{0};
+            struct timespec ts;
+            clock_gettime(CLOCK_REALTIME, &ts);
+            snprintf(I.shm_name, sizeof(I.shm_name), "/tpa_ipc_%d_%llu_%llx", (int)getpid(),
+                     (unsigned long long)seq++, (unsigned long long)ts.tv_nsec);
+            const int fd = shm_open(I.shm_name, O_CREAT | O_EXCL | O_RDWR, 0600);
+            if (fd < 0) throw std::runtime_error(std::string("shm_open failed: ") + I.shm_name);
+            I.shm_owner = true;
+            const int rc = ftruncate(fd, (off_t)I.shm_bytes);
+            void* p = rc == 0 ? mmap(nullptr, I.shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0) : MAP_FAILED;
+            close(fd);
+            if (p == MAP_FAILED) throw std::runtime_error("mapping the IPC stage counters failed");
+            I.shm = static_cast<volatile uint64_t*>(p);
+        }
+        std::memcpy(b.shm_name, I.shm_name, sizeof(b.shm_name));
+        std::memset(blob_out, 0, TPA_IPC_BLOB_BYTES);
+        std::memcpy(blob_out, &b, sizeof(b));
+        CK(cudaStreamSynchronize(g->stream));
+        *out = g.release();
+    });
+}
+
+int tpa_part_ipc_attach(tpa_graph* g, const void* blobs) {
+    return guard([&] {
+        if (!g || !blobs) throw std::invalid_argument("null argument");
+        if (!g->part || !g->part->ipc) throw std::invalid_argument("not an IPC partition");
+        PartInfo& P = *g->part;
+        IpcState& I = *P.ipc;
+        if (I.attached) throw std::invalid_argument("IPC partition already attached");
+        DeviceGuard dg(g->device);
+        const auto* all = static_cast<const unsigned char*>(blobs);
+        IpcBlob b0;
+        std::memcpy(&b0, all, sizeof(b0));
+        for (uint32_t r = 0; r < P.nranks; ++r) {
+            IpcBlob b;
+            std::memcpy(&b, all + (size_t)r * TPA_IPC_BLOB_BYTES, sizeof(b));
+            if (b.magic != kIpcMagic || b.nranks != P.nranks || b.rank != r ||
+                std::memcmp(b.shm_name, b0.shm_name, sizeof(b.shm_name)) != 0)
+                throw std::invalid_argument("IPC blobs are not one partitioning's, in rank order");
+            if (r == P.rank) continue;
+            IpcState::Peer& q = I.peers[r];
+            for (int k = 0; k < 2; ++k) {
+                void* p = nullptr;
+                CK(cudaIpcOpenMemHandle(&p, b.share[k], cudaIpcMemLazyEnablePeerAccess));
+                q.share[k] = static_cast<double*>(p);
+            }
+            void* pl = nullptr;
+            CK(cudaIpcOpenMemHandle(&pl, b.limbs, cudaIpcMemLazyEnablePeerAccess));
+            q.limbs = static_cast<unsigned long long*>(pl);
+            for (int k = 0; k < kIpcRing; ++k) CK(cudaIpcOpenEventHandle(&q.ev[k], b.ev[k]));
+        }
+        if (!I.shm_owner) {
+            std::memcpy(I.shm_name, b0.shm_name, sizeof(I.shm_name));
+            const int fd = shm_open(I.shm_name, O_RDWR, 0600);
+            if (fd < 0) throw std::runtime_error(std::string("shm_open failed: ") + I.shm_name);
+            void* p = mmap(nullptr, I.shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+            close(fd);
+            if (p == MAP_FAILED) throw std::runtime_error("mapping the IPC stage counters failed");
+            I.shm = static_cast<volatile uint64_t*>(p);
+        }
+        I.attached = true;
     });
 }
 

@@ -25,6 +25,7 @@ from .graph import Graph
 from .tpa import CpiParams, CpiResult, SeedSet, _terminal
 
 COMM_ID_BYTES = 128
+IPC_BLOB_BYTES = 1024  # TPA_IPC_BLOB_BYTES
 
 
 # SpMV tiling constants (csrc/cpi_kernels.cuh kMvTileNnz / kMvTileRows)
@@ -113,32 +114,63 @@ def _seed_args(seeds: SeedSet, n: int):
 
 
 class PartitionedGraph:
-    """Partition ``rank`` of ``nranks`` of ``g`` on ``device``; collective calls."""
+    """Partition ``rank`` of ``nranks`` of ``g`` on ``device``; collective calls.
 
-    def __init__(self, g: Graph, nranks: int, rank: int, comm_id: Optional[bytes] = None, device: int = 0):
+    transport "nccl": one in-place NCCL all-gather of the iterate's shares (and
+    the exact residual limbs) per sweep.  transport "ipc": the fused exchange --
+    every rank's sweep stores its shares straight into the peers' buffers
+    (CUDA IPC; ranks may share a device) -- built by ``create_ipc`` +
+    ``attach`` (``from_process_group`` does both)."""
+
+    def __init__(self, g: Graph, nranks: int, rank: int, comm_id: Optional[bytes] = None, device: int = 0,
+                 transport: str = "nccl"):
         h = C.c_void_p()
-        if comm_id is not None:
-            _prefer_torch_nccl()
-        idbuf = C.create_string_buffer(comm_id, COMM_ID_BYTES) if comm_id is not None else None
-        check(lib.tpa_graph_create_part(g.node_count(), g.edge_count(), g.out_offsets().ctypes.data,
-                                        g.out_targets().ctypes.data if g.edge_count() else None,
-                                        int(g.dangling_policy()), g.fingerprint(), int(device), int(nranks),
-                                        int(rank), idbuf, C.byref(h)))
+        self.blob = None
+        if transport == "ipc":
+            blob = C.create_string_buffer(IPC_BLOB_BYTES)
+            check(lib.tpa_graph_create_part_ipc(g.node_count(), g.edge_count(), g.out_offsets().ctypes.data,
+                                                g.out_targets().ctypes.data if g.edge_count() else None,
+                                                int(g.dangling_policy()), g.fingerprint(), int(device),
+                                                int(nranks), int(rank), blob, C.byref(h)))
+            self.blob = blob.raw
+        else:
+            if comm_id is not None:
+                _prefer_torch_nccl()
+            idbuf = C.create_string_buffer(comm_id, COMM_ID_BYTES) if comm_id is not None else None
+            check(lib.tpa_graph_create_part(g.node_count(), g.edge_count(), g.out_offsets().ctypes.data,
+                                            g.out_targets().ctypes.data if g.edge_count() else None,
+                                            int(g.dangling_policy()), g.fingerprint(), int(device), int(nranks),
+                                            int(rank), idbuf, C.byref(h)))
         self.h = h
         self.n = g.node_count()
         self.fingerprint = g.fingerprint()
+        self.transport = transport
+
+    def attach(self, blobs) -> None:
+        """IPC transport: every rank's export blob, in rank order."""
+        buf = b"".join(bytes(b) for b in blobs)
+        check(lib.tpa_part_ipc_attach(self.h, buf))
 
     @classmethod
-    def from_process_group(cls, g: Graph, device: Optional[int] = None, group=None) -> "PartitionedGraph":
-        """One partition per torch.distributed rank; rank 0's NCCL id is broadcast."""
+    def from_process_group(cls, g: Graph, device: Optional[int] = None, group=None,
+                           transport: str = "nccl") -> "PartitionedGraph":
+        """One partition per torch.distributed rank: rank 0's NCCL id broadcast,
+        or (transport "ipc") every rank's IPC blob all-gathered."""
         import torch.distributed as dist
         nranks, rank = dist.get_world_size(group), dist.get_rank(group)
-        obj = [comm_unique_id() if rank == 0 and nranks > 1 else None]
-        if nranks > 1:
-            dist.broadcast_object_list(obj, src=0, group=group)
         if device is None:
             import torch
             device = torch.cuda.current_device()
+        if transport == "ipc":
+            pg = cls(g, nranks, rank, None, device, transport="ipc")
+            blobs = [None] * nranks
+            dist.all_gather_object(blobs, pg.blob, group=group)
+            pg.attach(blobs)
+            dist.barrier(group=group)
+            return pg
+        obj = [comm_unique_id() if rank == 0 and nranks > 1 else None]
+        if nranks > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
         return cls(g, nranks, rank, obj[0], device)
 
     def info(self):
