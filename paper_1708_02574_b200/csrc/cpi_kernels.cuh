@@ -114,6 +114,112 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
     return r;
 }
 
+// ---- L2 residency (createpolicy + .L2::cache_hint) --------------------------
+// The sweeps gather the iterate at random while streaming everything else
+// (indices, row pointers, degrees, accumulators, outputs) once.  The streams
+// are marked evict_first so they do not displace the gathered iterate in the
+// 126 MB L2 (C4: 4.3 GB of acc / share / out traffic per B = 32 sweep).
+#ifndef TPA_HINT_STREAM
+#define TPA_HINT_STREAM 1
+#endif
+#ifndef TPA_HINT_GATHER  // iterate gathers: 0 evict_normal, 1 evict_last
+#define TPA_HINT_GATHER 0
+#endif
+#ifndef TPA_HINT_SHOUT  // next-iterate stores: 0 evict_normal, 1 evict_last, 2 evict_first
+#define TPA_HINT_SHOUT 0
+#endif
+struct L2Pol {
+    uint64_t first, last;
+};
+__device__ __forceinline__ L2Pol l2_policies() {
+    L2Pol p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.first));
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.last));
+    return p;
+}
+// read-once streams (never written by the kernel that reads them)
+__device__ __forceinline__ uint32_t ld_col(const uint32_t* p, const L2Pol& q) {
+    uint32_t r;
+#if TPA_HINT_STREAM
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(q.first));
+#else
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    (void)q;
+#endif
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_once_u32(const uint32_t* p, const L2Pol& q) {
+#if TPA_HINT_STREAM
+    uint32_t r;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(q.first));
+    return r;
+#else
+    (void)q;
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int64_t ld_once_s64(const int64_t* p, const L2Pol& q) {
+#if TPA_HINT_STREAM
+    int64_t r;
+    asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(q.first));
+    return r;
+#else
+    (void)q;
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_once_f64(const double* p, const L2Pol& q) {
+#if TPA_HINT_STREAM
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(q.first));
+    return r;
+#else
+    (void)q;
+    return __ldg(p);
+#endif
+}
+// the window accumulator: read, then written back by the same thread
+__device__ __forceinline__ double ld_acc(const double* p, const L2Pol& q) {
+#if TPA_HINT_STREAM
+    double r;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(q.first) : "memory");
+    return r;
+#else
+    (void)q;
+    return *p;
+#endif
+}
+__device__ __forceinline__ void st_stream(double* p, double v, const L2Pol& q) {
+#if TPA_HINT_STREAM
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(q.first) : "memory");
+#else
+    (void)q;
+    *p = v;
+#endif
+}
+// the next iterate (gathered by the next sweep)
+__device__ __forceinline__ void st_share(double* p, double v, const L2Pol& q) {
+#if TPA_HINT_SHOUT == 1
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(q.last) : "memory");
+#elif TPA_HINT_SHOUT == 2
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(q.first) : "memory");
+#else
+    (void)q;
+    *p = v;
+#endif
+}
+// one gathered iterate value (B = 1)
+__device__ __forceinline__ double ld_gather(const double* p, const L2Pol& q) {
+#if TPA_HINT_GATHER
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(q.last));
+    return r;
+#else
+    (void)q;
+    return __ldg(p);
+#endif
+}
+
 // Deterministic warp sum: xor butterfly, every lane ends with the same value.
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -249,39 +355,17 @@ template <> struct MmVec<16> { static constexpr int G = 16, CPL = 1; };
 template <> struct MmVec<32> { static constexpr int G = 32, CPL = 1; };
 template <> struct MmVec<64> { static constexpr int G = 32, CPL = 2; };
 
-// TPA_GATHER_HINT (A/B knob): 0 = plain LDG; 1 = L1::no_allocate (the row
-// gathers hit L1 ~4% of the time on dense sweeps); 2 = L1::evict_first;
-// 3 = L2::evict_last (keep the gathered share rows in L2 against the
-// streaming acc / share_out traffic).
-#ifndef TPA_GATHER_HINT
-#define TPA_GATHER_HINT 0
-#endif
+// One lane's CPL columns of a gathered share row (B >= 8).
 template <int CPL>
-__device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
-#if TPA_GATHER_HINT == 1
-#define TPA_GH_Q ".L1::no_allocate"
-#elif TPA_GATHER_HINT == 2
-#define TPA_GH_Q ".L1::evict_first"
-#endif
-#if TPA_GATHER_HINT == 3
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+__device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL], const L2Pol& q) {
+#if TPA_HINT_GATHER
     if constexpr (CPL == 1) {
-        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(pol));
+        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(q.last));
     } else {
-        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(q.last));
     }
-    return;
-#endif
-#ifdef TPA_GH_Q
-    if constexpr (CPL == 1) {
-        asm("ld.global.nc" TPA_GH_Q ".f64 %0, [%1];" : "=d"(v[0]) : "l"(p));
-    } else {
-        asm("ld.global.nc" TPA_GH_Q ".v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
-    }
-    return;
-#undef TPA_GH_Q
-#endif
+#else
+    (void)q;
     if constexpr (CPL == 1) {
         v[0] = __ldg(p);
     } else {
@@ -289,6 +373,7 @@ __device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
         v[0] = t.x;
         v[1] = t.y;
     }
+#endif
 }
 
 }  // namespace tpa

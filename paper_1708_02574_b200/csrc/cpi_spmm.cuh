@@ -274,7 +274,7 @@ __device__ __forceinline__ void consume_staged(const double* __restrict__ share,
             w[4 * q + 3] = t.w;
         }
 #pragma unroll
-        for (int j = 0; j < kU; ++j) ld_cols<CPL>(share + (size_t)w[j] * B + c0, v[j]);
+        for (int j = 0; j < kU; ++j) ld_cols<CPL>(share + (size_t)w[j] * B + c0, v[j], l2_policies());
     };
     auto consume = [&](int ci, const double (&v)[kU][CPL]) {
         const int base = ci * kU;

@@ -18,11 +18,6 @@
 
 namespace tpa {
 
-// TPA_EPI_STORE_HINT (A/B knob): epilogue acc / share_out stores as
-// streaming (evict-first) stores.
-#ifndef TPA_EPI_STORE_HINT
-#define TPA_EPI_STORE_HINT 0
-#endif
 // A/B knobs: an unpredicated gather group when all its sources are live;
 // the window's gather groups unrolled (shuffle lanes become immediates).
 #ifndef TPA_MM5_ALL_LIVE
@@ -67,12 +62,22 @@ struct Mm5 {
 };
 
 template <int CPL>
-__device__ __forceinline__ void cp_async_acc(double* dst_smem, const double* src) {
+__device__ __forceinline__ void cp_async_acc(double* dst_smem, const double* src, const L2Pol& q) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+#if TPA_HINT_STREAM
+    if constexpr (CPL == 1)
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(q.first)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "l"(q.first)
+                     : "memory");
+#else
+    (void)q;
     if constexpr (CPL == 1)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+#endif
 }
 
 template <int B, bool kLast, int RB>
@@ -117,6 +122,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         any_active = any_active || st[c].active;
     }
     any_active = __any_sync(0xffffffffu, any_active);
+    const L2Pol pol = l2_policies();
     const bool want_dm = a.policy == kUniform;
     unsigned long long fx[4][CPL];
 #pragma unroll
@@ -183,16 +189,16 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             const int64_t hi = min(lo + (int64_t)kLong, (int64_t)__ldg(a.row_ptr + r0 + 1));
             rpl = lane == 0 ? lo : hi;
         } else {
-            rpl = lane <= nrows ? __ldg(a.row_ptr + r0 + lane) : 0;
+            rpl = lane <= nrows ? ld_once_s64(a.row_ptr + r0 + lane, pol) : 0;
         }
         // block epilogue inputs, fetched now so they land during the gathers
         const uint32_t av = (A.acc_valid && a.acc) ? __ldcg(A.acc_valid + (r0 >> 5)) : 0u;
-        const uint32_t dl = lane < nrows ? __ldg(a.deg + r0 + lane) : 0u;
+        const uint32_t dl = lane < nrows ? ld_once_u32(a.deg + r0 + lane, pol) : 0u;
         if (!is_seg && a.acc) {
             // PAIR: each half-warp fetches the rows its epilogue takes
             for (int k = PAIR ? half : 0; k < nrows; k += PAIR ? 2 : 1)
                 if ((av >> ((r0 + k) & 31)) & 1u)
-                    cp_async_acc<CPL>(tile + k * TS + c0, a.acc + (size_t)(r0 + k) * B + c0);
+                    cp_async_acc<CPL>(tile + k * TS + c0, a.acc + (size_t)(r0 + k) * B + c0, pol);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
 
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         // U-wide gather groups take their sources from the window by shuffle
         auto idx32 = [&](int64_t base) -> uint32_t {
             const int64_t e = base + lane;
-            return e < e1 ? ld_stream_u32(col + e) : 0u;
+            return e < e1 ? ld_col(col + e, pol) : 0u;
         };
         auto bits32 = [&](uint32_t u, int64_t base) -> uint32_t {
 #if TPA_MM5_TIMING_NO_LIVE  // TIMING PROBE ONLY (wrong results): no frontier lookups
@@ -260,7 +266,12 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                         for (int jp = 0; jp < U / 2; ++jp) {
                             const int pp = 2 * jp + half;
                             const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + pp);
-                            v[jp] = ((lmask >> pp) & 1u) ? __ldg(share + (size_t)u * B + c0) : 0.0;
+                            v[jp] = 0.0;
+                            if ((lmask >> pp) & 1u) {
+                                double t1[1];
+                                ld_cols<1>(share + (size_t)u * B + c0, t1, pol);
+                                v[jp] = t1[0];
+                            }
                         }
                         // the term of position j: the lower half holds 2j'
                         // and receives 2j'+1 from the upper half, so its sum
@@ -304,14 +315,14 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
 #pragma unroll
                             for (int j = 0; j < U; ++j) {
                                 const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
-                                ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
+                                ld_cols<CPL>(share + (size_t)u * B + c0, v[j], pol);
                             }
                         } else {
 #pragma unroll
                             for (int j = 0; j < U; ++j) {
                                 const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
                                 if ((lmask >> j) & 1u) {
-                                    ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
+                                    ld_cols<CPL>(share + (size_t)u * B + c0, v[j], pol);
                                 } else {
 #pragma unroll
                                     for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 yb[0][c0 + c] = y;
             }
             if (lane == 0) A.long_cnt[li] = 0;
-            if (a.acc && ((av >> (r0 & 31)) & 1u)) cp_async_acc<CPL>(tile + c0, a.acc + (size_t)r0 * B + c0);
+            if (a.acc && ((av >> (r0 & 31)) & 1u)) cp_async_acc<CPL>(tile + c0, a.acc + (size_t)r0 * B + c0, pol);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         } else if (ne_mask) {
 #pragma unroll
@@ -430,13 +441,8 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                     tile[k * TS + c0 + c] = combine_value(a, f, r);  // tpa.cpp:73-74
                 } else {
                     const double sh = d ? ddiv(dmul(a.keep, yy[c]), (double)d) : 0.0;  // graph.cpp:222
-#if TPA_EPI_STORE_HINT
-                    __stcs(a.acc + ix, f);
-                    __stcs(a.share_out + ix, sh);
-#else
-                    a.acc[ix] = f;
-                    a.share_out[ix] = sh;
-#endif
+                    st_stream(a.acc + ix, f, pol);
+                    st_share(a.share_out + ix, sh, pol);
                 }
                 bl1[c] = dadd(bl1[c], fabs(yy[c]));
                 if (want_dm && d == 0) bdm[c] = dadd(bdm[c], yy[c]);
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 // transposed: RB lanes x 8 B contiguous of one seed's vector per store
                 const int k = lane % RB;
                 for (uint32_t b = lane / RB; b < a.b_valid; b += 32 / RB)
-                    if (k < nrows) a.out[(size_t)b * a.n + r0 + k] = tile[k * TS + b];
+                    if (k < nrows) st_stream(a.out + (size_t)b * a.n + r0 + k, tile[k * TS + b], pol);
             }
             __syncwarp();
         }

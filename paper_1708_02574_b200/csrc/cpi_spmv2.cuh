@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous sweep's shares, acc, state
 #endif
     const ColState st = a.state_in[0];
+    const L2Pol pol = l2_policies();
 
     if (!st.active) {
         // column stopped earlier: only a pending combine remains (tpa.cpp:73)
@@ -206,23 +207,23 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int k = tid + j * kThr;
-            u[j] = k < nnz ? ld_stream_u32(a.col + nb + k) : 0u;
+            u[j] = k < nnz ? ld_col(a.col + nb + k, pol) : 0u;
         }
-        for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(a.row_ptr[rb + r] - nb);
+        for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(ld_once_s64(a.row_ptr + rb + r, pol) - nb);
         uint32_t dg[RPT];
         double ac[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const uint32_t r = tid + q * kThr;
-            dg[q] = r < nrows ? __ldg(a.deg + rb + r) : 0u;
-            ac[q] = (r < nrows && a.acc) ? a.acc[rb + r] : 0.0;
+            dg[q] = r < nrows ? ld_once_u32(a.deg + rb + r, pol) : 0u;
+            ac[q] = (r < nrows && a.acc) ? ld_acc(a.acc + rb + r, pol) : 0.0;
         }
         // ---- round trip 2: gathers ----
         double v[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int k = tid + j * kThr;
-            v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
+            v[j] = k < nnz ? ld_gather(a.share_in + u[j], pol) : 0.0;
         }
 #if TPA_MV2_SEGSCAN
         // (A/B experiment, measured slower: C2 0.126-0.139 ms vs 0.110, C4
@@ -373,14 +374,15 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             if (a.acc) {
                 const double f = dadd(ac[q], y);  // cpi.cpp:50
                 if (a.out) {
-                    a.out[vtx] = a.stranger ? dadd(dmul(a.scale, f), a.stranger[vtx]) : dmul(f, a.scale);
+                    st_stream(a.out + vtx, a.stranger ? dadd(dmul(a.scale, f), ld_once_f64(a.stranger + vtx, pol))
+                                                      : dmul(f, a.scale), pol);
                 } else {
-                    a.acc[vtx] = f;
+                    st_stream(a.acc + vtx, f, pol);
                 }
             }
             if (a.share_out) {
                 const double sv = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
-                a.share_out[vtx] = sv;
+                st_share(a.share_out + vtx, sv, pol);
                 for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][vtx] = sv;
             }
             add_row(y, dg[q] == 0);
@@ -394,13 +396,13 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             uint32_t u[U];
             double v[U];
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = ld_stream_u32(a.col + e + j * kThr);
+            for (int j = 0; j < U; ++j) u[j] = ld_col(a.col + e + j * kThr, pol);
 #pragma unroll
-            for (int j = 0; j < U; ++j) v[j] = __ldg(a.share_in + u[j]);
+            for (int j = 0; j < U; ++j) v[j] = ld_gather(a.share_in + u[j], pol);
 #pragma unroll
             for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
         }
-        for (; e < ne; e += kThr) s = dadd(s, __ldg(a.share_in + ld_stream_u32(a.col + e)));
+        for (; e < ne; e += kThr) s = dadd(s, ld_gather(a.share_in + ld_col(a.col + e, pol), pol));
         s = mv_block_sum<kThr>(s, s_red);
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
