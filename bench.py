@@ -1,12 +1,15 @@
 #!/usr/bin/env python3
 """Benchmark of the CPI hot path (TPA preprocessing + batched online RWR queries).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
-One *step* is one pass of the hot path over one job of the chosen BASELINE
-config: PageRank preprocessing (the stranger vector, 116 sweeps at c=0.15,
-eps=1e-9) followed by the config's online queries (1,024 seeds at C2) in SpMM
-batches (32 at C2), S=5, T=10.  Inputs (graph CSR, seeds) are resident on the
+The default workload is BASELINE.json configs[3] (C4: R-MAT scale 24, edge
+factor 32, 529 M edges): the metric names no config, so the headline is the
+largest config that runs on one GPU (C5 is stated row-sharded over 2/4/8).
+One *step* is one pass of the hot path over one job of the chosen config:
+PageRank preprocessing (the stranger vector, 116 sweeps at c=0.15, eps=1e-9)
+followed by the config's online queries (1,024 seeds at C4) in SpMM batches
+(32 at C4), S=5, T=10.  Inputs (graph CSR, seeds) are resident on the
 device before the timed region; outputs stay in HBM.  Between timed steps the
 L2 is flushed (a 512 MiB write, outside the events).
 
@@ -15,8 +18,11 @@ m * (sweeps x active columns) per second -- with queries/s and the HBM
 roofline fraction of the dominant sweep kernel reported beside it.
 
 --impl reference times the reference's own CPU implementation
-(oracle/_ref/librwrank_ref.so, built from /root/reference/proj/src; the C
-oracle port if that is absent) on the host cores, same config and metric.
+(oracle/_ref/librwrank_ref.so, built from /root/reference/proj/src) on the
+host cores, same config and metric, importing nothing of the product: the
+graph comes from the reference's own Graph constructor fed by the benchmark
+generator restated in oracle/ref_capi.cpp (fingerprint printed in `config`,
+equal to our arm's), each step one bounded sample (RefCpuSampler).
 
 Multi-GPU (torchrun, one rank per GPU): the one job strong-scaled --
 PageRank preprocessing row-partitioned across the ranks (the fused exchange:
@@ -264,10 +270,12 @@ class RefCpuSampler:
     * preprocess: the whole preprocess() when it fits the budget, else
       116 x one dense propagation_sweep (graph.cpp:230-270) -- at the faster of
       threads = 1 and threads = min(cores, 64) (picked once, untimed);
-    * queries: a window of the job's seeds (>= 16, >= one per core) run as
+    * queries: a window of the job's seeds (one per core, at least 16) run as
       concurrent single-thread reference query() calls on every core
       (tpa_test.cpp:148-161: concurrent queries are the reference's contract),
-      a different window each step."""
+      a different window each step.
+    A C4 step is then ~12 s of CPU work (one 2.2 s sweep + 16 concurrent
+    6-8 s queries), so a 20-step run stays within a few minutes."""
 
     def __init__(self, rg, seeds, budget_s=20.0, workers=None):
         self.rg, self.seeds = rg, np.ascontiguousarray(seeds, np.uint32)
@@ -284,9 +292,7 @@ class RefCpuSampler:
         self.stranger = np.zeros(self.n)
         if self.whole_pre:
             self.stranger = rg.preprocess(C, EPS, T, self.pre_threads)
-        est_q = max(t_sw * 1.2, 1e-4)  # a query: 4 sweeps with the zero-skip
-        k = int(budget_s * 0.5 / est_q * self.workers)
-        self.qs = int(min(self.nq, max(16, self.workers, k)))
+        self.qs = int(min(self.nq, max(16, self.workers)))
         self.cursor = 0
 
     def step(self):
@@ -317,10 +323,8 @@ class RefCpuSampler:
 
 
 def cpu_measure(rg, seeds, budget_s=20.0):
-    """cpu_baseline of the GPU arm: one bounded reference sample (after an
-    untimed one)."""
+    """cpu_baseline of the GPU arm: one bounded reference sample."""
     smp = RefCpuSampler(rg, seeds, budget_s)
-    smp.step()
     return smp.baseline([smp.step()])
 
 
@@ -339,11 +343,11 @@ def run_reference_arm(args):
     log(f"[reference] graph {cfg_name}: n={rg.n} m={rg.m} built in {t_build:.1f}s")
     seeds = rg.sample_seeds(nq, seed)
     smp = RefCpuSampler(rg, seeds, budget_s=args.cpu_budget)
-    recs = []
-    for i in range(max(0, args.warmup) + max(1, args.steps)):
-        r = smp.step()
-        if i >= args.warmup:
-            recs.append(r)
+    # warm-up steps: one dense sweep each (the CPU path has nothing to compile
+    # or tune; this only warms caches and page tables)
+    for _ in range(max(0, args.warmup)):
+        rg.time_sweeps(1, C, smp.pre_threads)
+    recs = [smp.step() for _ in range(max(1, args.steps))]
     cb = smp.baseline(recs)
     v = cb["value"]
     line = {"impl": "reference", "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",

@@ -44,3 +44,24 @@ def test_gpu_arm_line():
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert 0 < r["frac"] < 1
     assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["clocks"]["samples"] > 0
+
+
+def test_reference_arm_imports_no_product_code():
+    """--impl reference must time the reference alone: nothing of the product
+    package (nor its libtpa_gpu.so) is loaded in that process."""
+    from oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    code = (
+        "import runpy, sys\n"
+        "sys.argv = ['bench.py', '--impl', 'reference', '--config', 'c1', '--steps', '1', '--warmup', '0']\n"
+        "try:\n"
+        "    runpy.run_path('bench.py', run_name='__main__')\n"
+        "except SystemExit:\n"
+        "    pass\n"
+        "bad = [m for m in sys.modules if m.startswith('paper_1708_02574_b200')]\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "assert not bad and 'libtpa_gpu' not in maps, bad\n"
+        "print('clean')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and "clean" in r.stdout, r.stderr[-2000:]
