@@ -120,7 +120,7 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
 // are marked evict_first so they do not displace the gathered iterate in the
 // 126 MB L2 (C4: 4.3 GB of acc / share / out traffic per B = 32 sweep).
 #ifndef TPA_HINT_STREAM
-#define TPA_HINT_STREAM 1
+#define TPA_HINT_STREAM 0
 #endif
 #ifndef TPA_HINT_GATHER  // iterate gathers: 0 evict_normal, 1 evict_last
 #define TPA_HINT_GATHER 0

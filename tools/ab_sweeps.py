@@ -14,8 +14,8 @@ sys.path.append(ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import paper_1708_02574_b200 as P  # noqa: E402  (the variant on PYTHONPATH, before bench adds ROOT)
 import bench  # noqa: E402
-import paper_1708_02574_b200 as P  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")

@@ -5,9 +5,16 @@
 //   B: cp.async.bulk (bulk-copy / TMA engine) of whole rows into a per-warp
 //      shared-memory ring, one row per lane per instruction, mbarrier-tracked
 //   C: cp.async (LDGSTS) 16 B per lane into the same ring
+//   D: TMA tile::gather4 (cp.async.bulk.tensor.2d ... gather4): one request
+//      fetches FOUR rows named by four indices (tensor map over [n][32] f64,
+//      box 32 x 1); per warp a ring of S stages x 32 rows, lanes 0-7 issue
+//      the 8 gather4 requests of a stage
+// argv[1] = rows of X (default 2^20: 268 MB, partly L2-resident; 16777216 is
+// C4's 4.3 GB share matrix)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_micro tools/gather_micro.cu
 #include <cstdint>
 #include <cstdio>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <vector>
 #include <random>
@@ -95,6 +102,54 @@ __global__ void gather_bulk(const double* __restrict__ X, const uint32_t* __rest
 }
 
 
+// D: TMA gather4
+template <int S>
+__global__ void gather_g4(const __grid_constant__ CUtensorMap tm, const uint32_t* __restrict__ idx, long long m,
+                          double* out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem) + (size_t)w * S * 32 * B;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nwb * S * 32 * B * 8) + w * S;
+    if (lane < S) mbar_init(&bars[lane], 1);
+    __syncwarp();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = ((m + nw - 1) / nw + 31) / 32 * 32;
+    const long long lo = warp * per, hi = min(m, lo + per);
+    const long long nst = (hi > lo) ? (hi - lo + 31) / 32 : 0;
+    auto issue = [&](long long k) {
+        if (k >= nst) return;
+        const int slot = (int)(k % S);
+        const long long e = lo + k * 32 + lane;
+        const uint32_t myi = e < hi ? __ldg(idx + e) : 0u;  // tail: row 0 (counted, harmless)
+        const int q = lane * 4;
+        const int r0 = __shfl_sync(0xffffffffu, myi, q & 31), r1 = __shfl_sync(0xffffffffu, myi, (q + 1) & 31);
+        const int r2 = __shfl_sync(0xffffffffu, myi, (q + 2) & 31), r3 = __shfl_sync(0xffffffffu, myi, (q + 3) & 31);
+        if (lane == 0) mbar_expect_tx(&bars[slot], 32 * B * 8);
+        __syncwarp();
+        if (lane < 8) {
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(ring + ((size_t)slot * 32 + q) * B);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d), "l"(&tm), "r"(0), "r"(r0), "r"(r1), "r"(r2),
+                "r"(r3), "r"((uint32_t)__cvta_generic_to_shared(&bars[slot]))
+                : "memory");
+        }
+    };
+    for (int k = 0; k < S; ++k) issue(k);
+    double s = 0.0;
+    for (long long k = 0; k < nst; ++k) {
+        const int slot = (int)(k % S);
+        mbar_wait(&bars[slot], (uint32_t)((k / S) & 1));
+        const int cnt = (int)min(32LL, hi - (lo + k * 32));
+        for (int j = 0; j < cnt; ++j) s += ring[((size_t)slot * 32 + j) * B + lane];
+        __syncwarp();
+        issue(k + S);
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
 // C: cp.async 16 B per lane into a per-warp ring of S stages x R rows; lane
 // pair (2 rows per instruction: lanes 0-15 row a, 16-31 row b), consumer reads
 // lane = column (8 B) per row.
@@ -144,7 +199,7 @@ __global__ void gather_ldgsts(const double* __restrict__ X, const uint32_t* __re
 }
 
 int main(int argc, char** argv) {
-    const uint32_t n = 1 << 20;
+    const uint32_t n = argc > 1 ? (uint32_t)atoll(argv[1]) : (1u << 20);
     const long long m = 16586831;
     double* X;
     uint32_t* idx;
@@ -158,7 +213,7 @@ int main(int argc, char** argv) {
     // skewed like R-MAT: mix of hub-heavy and uniform sources
     for (long long i = 0; i < m; ++i) {
         const double r = (rng() >> 11) * 0x1p-53;
-        h[i] = r < 0.5 ? (uint32_t)(rng() % 16384) : (uint32_t)(rng() % n);
+        h[i] = r < 0.5 ? (uint32_t)(rng() % (n / 64)) : (uint32_t)(rng() % n);
     }
     CK(cudaMemcpy(idx, h.data(), m * 4, cudaMemcpyHostToDevice));
     int sms = 148;
@@ -199,11 +254,55 @@ int main(int argc, char** argv) {
     ring(gather_ldgsts<6, 8>, 6, 8, 4);
     ring(gather_ldgsts<8, 8>, 8, 8, 2);
     ring(gather_ldgsts<3, 32>, 3, 32, 2);
+    printf("X: %u rows (%.0f MB)\n", n, n * 256.0 / 1e6);
+    {
+        // tensor map over X as [n][32] f64, box 32 x 1 (gather4 takes 4 rows)
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        auto enc = reinterpret_cast<CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                                 CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                                 CUtensorMapFloatOOBfill)>(fn);
+        CUtensorMap tm;
+        cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)n};
+        cuuint64_t strides[1] = {(cuuint64_t)B * 8};
+        cuuint32_t box[2] = {(cuuint32_t)B, 1};
+        cuuint32_t es[2] = {1, 1};
+        for (auto prom : {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B}) {
+            CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, X, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                printf("cuTensorMapEncodeTiled failed %d\n", (int)r);
+                break;
+            }
+            for (int S : {2, 4}) {
+                for (int wpb : {4, 8}) {
+                    const size_t smem = (size_t)wpb * S * 32 * B * 8 + wpb * S * 8;
+                    auto k = S == 2 ? gather_g4<2> : gather_g4<4>;
+                    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+                        cudaGetLastError();
+                        continue;
+                    }
+                    int occ = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, wpb * 32, smem);
+                    if (occ < 1) continue;
+                    char nm[80];
+                    snprintf(nm, 80, "gather4 S=%d %dw x %d CTA/SM prom%d", S, wpb, occ, (int)prom);
+                    timeit(nm, [&] { k<<<sms * occ, wpb * 32, smem>>>(tm, idx, m, out); });
+                }
+            }
+        }
+    }
     for (int S : {2, 4}) {
         for (int wpb : {4, 8}) {
             const size_t smem = (size_t)wpb * S * 32 * B * 8 + wpb * S * 8;
             auto k = S == 2 ? gather_bulk<2> : gather_bulk<4>;
-            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
             int occ = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, wpb * 32, smem);
             char nm[80];
