@@ -71,6 +71,7 @@ struct StepArgs {
     const int64_t* __restrict__ row_ptr;  // CSR(Ãᵀ) n+1
     const uint32_t* __restrict__ col;     // m, ascending per row
     const uint32_t* __restrict__ deg;     // out-degree per node (n)
+    const uint32_t* __restrict__ rank;    // B = 1 ranked layout: share slot of node v (null: v)
     const uint2* __restrict__ items;      // {row_begin, row_end | kLongFlag}
     uint32_t n_items;
     uint32_t n;

@@ -210,12 +210,13 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             u[j] = k < nnz ? ld_col(a.col + nb + k, pol) : 0u;
         }
         for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(ld_once_s64(a.row_ptr + rb + r, pol) - nb);
-        uint32_t dg[RPT];
+        uint32_t dg[RPT], so[RPT];
         double ac[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const uint32_t r = tid + q * kThr;
             dg[q] = r < nrows ? ld_once_u32(a.deg + rb + r, pol) : 0u;
+            so[q] = (r < nrows && a.rank) ? ld_once_u32(a.rank + rb + r, pol) : rb + r;  // share slot
             ac[q] = (r < nrows && a.acc) ? ld_acc(a.acc + rb + r, pol) : 0.0;
         }
         // ---- round trip 2: gathers ----
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             }
             if (a.share_out) {
                 const double sv = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
-                st_share(a.share_out + vtx, sv, pol);
+                st_share(a.share_out + so[q], sv, pol);
                 for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][vtx] = sv;
             }
             add_row(y, dg[q] == 0);
@@ -406,9 +407,19 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         s = mv_block_sum<kThr>(s, s_red);
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
-            const double y = epilogue(a, st, rb, 0, 1, rb, s, d);
-            if (a.share_out)
-                for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][rb] = d ? ddiv(dmul(a.keep, y), (double)d) : 0.0;
+            double y = s;
+            if (st.has_spread) y = dadd(y, st.spread);  // graph.cpp:265-268
+            if (a.y_out) a.y_out[rb] = y;
+            if (a.acc) {
+                const double f = dadd(a.acc[rb], y);  // cpi.cpp:50
+                if (a.out) a.out[rb] = a.stranger ? dadd(dmul(a.scale, f), a.stranger[rb]) : dmul(f, a.scale);
+                else a.acc[rb] = f;
+            }
+            if (a.share_out) {
+                const double sv = d ? ddiv(dmul(a.keep, y), (double)d) : 0.0;  // graph.cpp:222
+                a.share_out[a.rank ? a.rank[rb] : rb] = sv;
+                for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][rb] = sv;
+            }
             add_row(y, d == 0);
         }
     }

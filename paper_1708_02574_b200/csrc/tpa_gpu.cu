@@ -135,6 +135,30 @@ struct DevBuf {
     }
 };
 
+// Ranked share layout (B = 1 sweeps): node u's share lives at slot rank[u],
+// nodes ordered by out-degree, descending (ties by id).  The hot sources --
+// C4: the top 10% of nodes feed 89% of the gathers -- then share 32-byte
+// sectors and L2 lines instead of being spread over the whole vector.
+#ifndef TPA_RANKED
+#define TPA_RANKED 1
+#endif
+__global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint32_t n, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ ids) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
+        keys[u] = ~deg[u];
+        ids[u] = (uint32_t)u;
+    }
+}
+__global__ void k_rank_scatter(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* __restrict__ rank) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+        rank[perm[k]] = (uint32_t)k;
+}
+__global__ void k_col_rank(const uint32_t* __restrict__ col, uint64_t m, const uint32_t* __restrict__ rank,
+                           uint32_t* __restrict__ col_rank) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+        col_rank[e] = __ldg(rank + col[e]);
+}
+
 // ---------------------------------------------------------------------------
 // K1: ingest -- out-edge CSR -> CSR(Ãᵀ) (stable radix sort by target keeps
 // sources ascending inside every row: the reference's scatter order).
@@ -179,7 +203,8 @@ __global__ void k_row_ptr(const uint32_t* __restrict__ keys, uint64_t m, uint32_
 __global__ void __launch_bounds__(kThreads)
 k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
              const uint32_t* __restrict__ deg, double keep, double* __restrict__ share0,
-             double* __restrict__ acc0, unsigned long long* fx, double* __restrict__ dm_part) {
+             double* __restrict__ acc0, unsigned long long* fx, double* __restrict__ dm_part,
+             const uint32_t* __restrict__ rank) {
     __shared__ unsigned long long s_w[4 * (kThreads / 32)];
     __shared__ double s_dm[kThreads / 32];
     unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
@@ -187,7 +212,7 @@ k_init_dense(const double* __restrict__ x, double weight, uint32_t n,
     for (uint64_t u = blockIdx.x * (uint64_t)kThreads + threadIdx.x; u < n; u += (uint64_t)gridDim.x * kThreads) {
         const double xv = x ? x[u] : weight;
         const uint32_t d = deg[u];
-        share0[u] = d ? ddiv(dmul(keep, xv), (double)d) : 0.0;
+        share0[rank ? rank[u] : u] = d ? ddiv(dmul(keep, xv), (double)d) : 0.0;
         if (acc0) acc0[u] = xv;
         fx_add(f0, f1, xv);
         if (d == 0) {
@@ -247,7 +272,7 @@ __global__ void k_init_finish(unsigned long long* fx, unsigned long long* limbs,
 __global__ void k_init_seeds(const SeedList seeds, uint32_t b_valid, int B, double c,
                              double keep, uint32_t n, int policy, const uint32_t* __restrict__ deg,
                              double* __restrict__ share0, double* __restrict__ acc0, int active0,
-                             ColState* state0) {
+                             ColState* state0, const uint32_t* __restrict__ rank) {
     const int b = threadIdx.x;
     if (b >= B) return;
     ColState s;
@@ -257,7 +282,7 @@ __global__ void k_init_seeds(const SeedList seeds, uint32_t b_valid, int B, doub
         const uint32_t seed = seeds.s[b];
         const uint32_t d = deg[seed];
         const double w = c;  // c / |S| with |S| = 1
-        share0[(size_t)seed * B + b] = d ? ddiv(dmul(keep, w), (double)d) : 0.0;
+        share0[(size_t)(rank ? rank[seed] : seed) * B + b] = d ? ddiv(dmul(keep, w), (double)d) : 0.0;  // rank: B = 1
         if (acc0) acc0[(size_t)seed * B + b] = w;
         s.residual = w;
         s.active = active0;
@@ -512,6 +537,10 @@ struct tpa_graph {
     int policy = 0;
     uint64_t fingerprint = 0;
     DevBuf row_ptr, col, deg;
+    // ranked layout of the B = 1 sweeps (PageRank, single-vector CPI): nodes
+    // numbered by out-degree (descending) in the share vector only -- rows stay
+    // in id order; col_rank = rank[col]; empty when not built (small graphs)
+    DevBuf rank, col_rank;
     DevBuf out_off, out_tgt;  // the out-edge CSR itself (frontier push-marking)
     Schedule mv;  // SpMV work items
     MvShape mv_shape = kMvShapeS;  // SpMV tile shape (mv_shape of the global node count)
@@ -891,6 +920,8 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const bool partition = !cfg.bounds.empty() || !cfg.seg_acc.empty();
     double* acc_run = cfg.acc;
     const uint32_t* const deg_run = g->deg.as<uint32_t>();
+    // B = 1 over the ranked share layout when the graph has one (rows unchanged)
+    const uint32_t* const rank = (B == 1 && !partition && g->rank.p) ? g->rank.as<uint32_t>() : nullptr;
 
     // accumulator for x⁽⁰⁾, zero the rest
     double* acc0 = nullptr;
@@ -919,7 +950,7 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
         }
         k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.d_x, cfg.weight, n, deg_run, keep,
                                                        w.share[0].as<double>(), acc0,
-                                                       w.fx.as<unsigned long long>(), dm_part);
+                                                       w.fx.as<unsigned long long>(), dm_part, rank);
         CKL("k_init_dense");
         k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), nullptr, g->policy, keep, n,
                                               active0, st, dm_part, nblk);
@@ -938,14 +969,15 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
         CK(cudaMemsetAsync(w.share[0].p, 0, (size_t)n * B * 8, g->stream));
         k_init_seeds<<<1, 64, 0, g->stream>>>(cfg.seeds, cfg.b_valid, B, cfg.c, keep, n, g->policy,
                                               g->deg.as<uint32_t>(), w.share[0].as<double>(), acc0,
-                                              active0, st);
+                                              active0, st, rank);
         CKL("k_init_seeds");
         g->launches += 1;
     }
 
     StepArgs a{};
     a.row_ptr = g->row_ptr.as<int64_t>();
-    a.col = g->col.as<uint32_t>();
+    a.col = rank ? g->col_rank.as<uint32_t>() : g->col.as<uint32_t>();
+    a.rank = rank;
     a.deg = deg_run;
     a.items = sch.items.as<uint2>();
     a.n_items = sch.n_items;
@@ -1338,6 +1370,33 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         g->out_off.swap(d_off);  // the uploaded offsets are the out-CSR's
         CKL("k_row_ptr");
         d_keys.release();
+        // the ranked layout of the B = 1 sweeps, for share vectors beyond half
+        // the L2 (C4: 134 MB, C5: 2.1 GB), if the column copy fits comfortably
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        if (TPA_RANKED && m && (uint64_t)n * 8 > (64ull << 20) && m * 4 + (uint64_t)n * 24 < free_b / 2) {
+            DevBuf keys, keys2, ids, perm, tmp;
+            keys.ensure((size_t)n * 4, s);
+            keys2.ensure((size_t)n * 4, s);
+            ids.ensure((size_t)n * 4, s);
+            perm.ensure((size_t)n * 4, s);
+            k_rank_keys<<<blocks, 256, 0, s>>>(g->deg.as<uint32_t>(), n, keys.as<uint32_t>(), ids.as<uint32_t>());
+            CKL("k_rank_keys");
+            size_t temp = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                               ids.as<uint32_t>(), perm.as<uint32_t>(), (int64_t)n, 0, 32, s));
+            tmp.ensure(temp, s);
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, temp, keys.as<uint32_t>(), keys2.as<uint32_t>(),
+                                               ids.as<uint32_t>(), perm.as<uint32_t>(), (int64_t)n, 0, 32, s));
+            g->rank.ensure((size_t)n * 4, g->stream);  // (DevBuf keeps the stream variable's address)
+            k_rank_scatter<<<blocks, 256, 0, s>>>(perm.as<uint32_t>(), n, g->rank.as<uint32_t>());
+            CKL("k_rank_scatter");
+            g->col_rank.ensure(m * 4, g->stream);
+            k_col_rank<<<blocks, 256, 0, s>>>(g->col.as<uint32_t>(), m, g->rank.as<uint32_t>(),
+                                             g->col_rank.as<uint32_t>());
+            CKL("k_col_rank");
+            g->launches += 3;
+        }
         std::vector<int64_t> rp(n + 1ull);
         CK(cudaMemcpyAsync(rp.data(), g->row_ptr.p, (n + 1ull) * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1360,6 +1419,8 @@ int tpa_graph_destroy(tpa_graph* g) {
             g->ws.clear();
             g->row_ptr.release();
             g->col.release();
+            g->rank.release();
+            g->col_rank.release();
             g->deg.release();
             g->out_off.release();
             g->out_tgt.release();
@@ -1431,7 +1492,7 @@ int tpa_graph_info(const tpa_graph* g, uint32_t* n, uint64_t* m, uint64_t* finge
         if (fingerprint) *fingerprint = g->fingerprint;
         if (policy) *policy = g->policy;
         if (device_bytes) {
-            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->deg.bytes + g->mv.items.bytes + g->longs.seg_lo.bytes * 2 +
+            uint64_t b = g->row_ptr.bytes + g->col.bytes + g->rank.bytes + g->col_rank.bytes + g->deg.bytes + g->mv.items.bytes + g->longs.seg_lo.bytes * 2 +
                          g->out_off.bytes + g->out_tgt.bytes;
             for (auto& kv : g->ws) {
                 const Workspace& w = *kv.second;

@@ -445,7 +445,7 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
             k_init_dense<<<nblk, kThreads, 0, g->stream>>>(cfg.seeds ? dx[k].as<double>() : nullptr, weight, nl,
                                                            g->deg.as<uint32_t>(), keep,
                                                            w.share[0].as<double>() + (size_t)P.rank * P.stride,
-                                                           acc0, w.fx.as<unsigned long long>(), nullptr);
+                                                           acc0, w.fx.as<unsigned long long>(), nullptr, nullptr);
             CKL("k_init_dense");
         }
         k_init_finish<<<1, 1, 0, g->stream>>>(w.fx.as<unsigned long long>(), limbs_at(g, 2, 0), g->policy, keep,

@@ -22,13 +22,16 @@ ap.add_argument("--config", default="c4")
 ap.add_argument("--batches", type=int, default=4)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--tag", default=os.environ.get("PYTHONPATH", "product"))
+ap.add_argument("--no-queries", action="store_true", help="PageRank sweeps only (C5: no [B][n] output)")
 a = ap.parse_args()
 _, _, nq, B, seed = bench.CONFIGS[a.config]
 g = bench.build_graph(a.config)
 dg = g.device(0)
 art = P.preprocess(g, 0.15, 1e-9, 10)
-seeds = P.sample_seeds(g, B * a.batches, 1)
-out = torch.empty((B, g.node_count()), dtype=torch.float64, device="cuda")
+if a.no_queries:
+    a.batches = 0
+seeds = P.sample_seeds(g, B * max(a.batches, 1), 1)
+out = torch.empty((B, g.node_count()), dtype=torch.float64, device="cuda") if a.batches else None
 for k in range(a.batches):  # warm
     P.query_batch(g, art, seeds[k * B:(k + 1) * B], 5, out=out)
 torch.cuda.synchronize()
