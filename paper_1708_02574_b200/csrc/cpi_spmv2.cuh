@@ -99,11 +99,11 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
     return s;
 }
 
-// kRowFx = false: the residual / dangling mass as per-tile fixed-tree double
-// sums, added across tiles in exact fixed point (the totals depend on the
-// tiling only; a row partition cuts at tile starts, tpa_part.cuh).
-// kRowFx = true (the relabelled twin, tpa_relabel.cuh): every row's |y| goes
-// into exact fixed point on its own, so any tiling gives the same totals.
+// The residual / dangling mass are per-tile fixed-tree double sums, added
+// across tiles in exact fixed point (the totals depend on the tiling only; a
+// row partition cuts at tile starts, tpa_part.cuh).
+// kRanked: the ranked share layout (a.rank, tpa_gpu.cu): each share is stored
+// at its node's rank slot; gathers already read col_rank.
 
 // Deterministic CTA sum over kThr threads (fixed tree); valid in every thread.
 template <int kThr>
@@ -131,10 +131,10 @@ constexpr int kMvFxSlots = TPA_MV2_FX_SLOTS;  // [4 x slots] fixed-point accumul
 #define TPA_MV2_EARLY_EXIT 1
 #endif
 #ifdef TPA_MV2_MINB  // A/B knob; the default (no minimum) compiles to 40 registers, 6 CTAs/SM
-template <bool kRowFx, int kThr, int kNnz, int kRows>
+template <bool kRanked, int kThr, int kNnz, int kRows>
 __global__ void __launch_bounds__(kThr, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
 #else
-template <bool kRowFx, int kThr, int kNnz, int kRows>
+template <bool kRanked, int kThr, int kNnz, int kRows>
 __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
 #endif
     const StepArgs& a = M.s;
@@ -180,21 +180,10 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         return;
     }
     const bool want_dm = a.policy == kUniform;
-    // |y| and the dangling mass go into exact 128-bit fixed point ROW BY ROW:
-    // the totals are then independent of how rows are grouped into tiles (a
-    // row partition, or the relabelled twin of tpa_relabel.cuh, reproduces
-    // them bit for bit)
-    unsigned long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
-    __shared__ unsigned long long s_w[4 * (kThr / 32)];
     double my_l1 = 0.0, my_dm = 0.0;
     auto add_row = [&](double y, bool dangling) {
-        if constexpr (kRowFx) {
-            fx_add(f0, f1, y);
-            if (want_dm && dangling) fx_add(f2, f3, y);
-        } else {
-            my_l1 = dadd(my_l1, fabs(y));
-            if (want_dm && dangling) my_dm = dadd(my_dm, y);
-        }
+        my_l1 = dadd(my_l1, fabs(y));
+        if (want_dm && dangling) my_dm = dadd(my_dm, y);
     };
 
     if (!is_long) {
@@ -216,7 +205,8 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         for (int q = 0; q < RPT; ++q) {
             const uint32_t r = tid + q * kThr;
             dg[q] = r < nrows ? ld_once_u32(a.deg + rb + r, pol) : 0u;
-            so[q] = (r < nrows && a.rank) ? ld_once_u32(a.rank + rb + r, pol) : rb + r;  // share slot
+            if constexpr (kRanked) so[q] = r < nrows ? ld_once_u32(a.rank + rb + r, pol) : 0u;  // share slot
+            else so[q] = rb + r;
             ac[q] = (r < nrows && a.acc) ? ld_acc(a.acc + rb + r, pol) : 0.0;
         }
         // ---- round trip 2: gathers ----
@@ -417,16 +407,13 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             }
             if (a.share_out) {
                 const double sv = d ? ddiv(dmul(a.keep, y), (double)d) : 0.0;  // graph.cpp:222
-                a.share_out[a.rank ? a.rank[rb] : rb] = sv;
+                a.share_out[kRanked ? a.rank[rb] : rb] = sv;
                 for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][rb] = sv;
             }
             add_row(y, d == 0);
         }
     }
-    if constexpr (kRowFx) {
-        // exact CTA totals -> the sweep's totals (order-free integer sums)
-        fx_cta_flush(f0, f1, f2, f3, s_w, M.fx);
-    } else {
+    {
         // tile partials (fixed tree) -> exact fixed-point totals across tiles
         const double tl1 = mv_block_sum<kThr>(my_l1, s_red);
         const double tdm = want_dm ? mv_block_sum<kThr>(my_dm, s_red) : 0.0;

@@ -432,9 +432,8 @@ static void launch_fused(const Mm4Args& P, int num_sms, cudaStream_t stream) {
 
 template <int B, bool L>
 static void launch_fused_rb(const Mm4Args& P, int rb, int num_sms, cudaStream_t stream) {
-    if (rb == 4) launch_fused<B, L, 4>(P, num_sms, stream);
-    else if (rb == 8) launch_fused<B, L, 8>(P, num_sms, stream);
-    else launch_fused<B, L, 16>(P, num_sms, stream);
+    (void)rb;  // mm5_rows(B): 16 for B = 16, 8 otherwise
+    launch_fused<B, L, B == 16 ? 16 : 8>(P, num_sms, stream);
 }
 
 // Sweeps (of a seed batch) run frontier-driven: push-mark then pull.
@@ -884,10 +883,14 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                          PeerOut{}, g->part ? g->part->slice : 0u};
                 if (g->part && a.share_out) M.peers = g->peer_out;
                 const MvShape& sh = g->mv_shape;
-                if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows)
-                    launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
-                else
-                    launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
+                const bool ranked = a.rank != nullptr;
+                if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows) {
+                    if (ranked) launch_mv2<true, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
+                    else launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
+                } else {
+                    if (ranked) launch_mv2<true, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
+                    else launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
+                }
             }
             break;
         case 8: k_step_spmm2<8><<<grid, MmShape<8>::NT, MmShape<8>::kDynSmem, g->stream>>>(*mm); break;
