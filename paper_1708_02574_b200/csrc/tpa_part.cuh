@@ -784,8 +784,8 @@ int tpa_part_ipc_attach(tpa_graph* g, const void* blobs) {
         for (uint32_t r = 0; r < P.nranks; ++r) {
             IpcBlob b;
             std::memcpy(&b, all + (size_t)r * TPA_IPC_BLOB_BYTES, sizeof(b));
-            if (b.magic != kIpcMagic || b.nranks != P.nranks || b.rank != r ||
-                std::memcmp(b.shm_name, b0.shm_name, sizeof(b.shm_name)) != 0)
+            // (only rank 0's blob names the stage counters: it created them)
+            if (b.magic != kIpcMagic || b.nranks != P.nranks || b.rank != r || b0.shm_name[0] != '/')
                 throw std::invalid_argument("IPC blobs are not one partitioning's, in rank order");
             if (r == P.rank) continue;
             IpcState::Peer& q = I.peers[r];

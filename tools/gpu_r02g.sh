@@ -1,10 +1,9 @@
 #!/bin/bash
-# round-2 bench lines: C4 headline (driver args) + reference arm, then C2/C3/C1 lines
+# round-2 final pass: full -m gpu suite, C4 headline (driver args) + reference arm, C2 line
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
-/usr/bin/time -f "wall %e s" timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench_c4.json 2> gpurun_out/r02_bench_c4.err; echo "c4 rc $?"; tail -1 gpurun_out/r02_bench_c4.err
-/usr/bin/time -f "wall %e s" timeout 1500 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02_ref_c4.json 2> gpurun_out/r02_ref_c4.err; echo "ref rc $?"; tail -1 gpurun_out/r02_ref_c4.err
-for c in c2 c3 c1; do
-  timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/r02_bench_$c.json 2> gpurun_out/r02_bench_$c.err; echo "$c rc $?"
-done
+t0=$(date +%s); timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=12 > gpurun_out/r02_pytest_gpu.log 2>&1; echo "pytest rc $? $(( $(date +%s) - t0 ))s"; tail -2 gpurun_out/r02_pytest_gpu.log
+t0=$(date +%s); timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench_c4.json 2> gpurun_out/r02_bench_c4.err; echo "c4 rc $? $(( $(date +%s) - t0 ))s"
+t0=$(date +%s); timeout 1500 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02_ref_c4.json 2> gpurun_out/r02_ref_c4.err; echo "ref rc $? $(( $(date +%s) - t0 ))s"
+timeout 900 python bench.py --config c2 --steps 10 --warmup 3 --no-cpu > gpurun_out/r02_bench_c2.json 2> gpurun_out/r02_bench_c2.err; echo "c2 rc $?"
