@@ -21,7 +21,6 @@ struct Mm4Args {
     const uint32_t* __restrict__ win_blk;
     const uint32_t* __restrict__ sl;  // segments of the marked long rows
     const uint32_t* sl_cnt;
-    int tma;  // k_mm_tma takes the dense sweeps (cpi_spmm_tma.cuh): K3 runs the sparse ones only
 };
 
 // Direction-optimised sparse sweeps.  A frontier row is a row of share_in

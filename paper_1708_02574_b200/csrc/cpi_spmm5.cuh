@@ -87,7 +87,6 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     constexpr bool PAIR = Sh::PAIR;
     const MmArgs& A = P.m;
     const StepArgs& a = A.s;
-    if (P.tma && (P.rowflag == nullptr || *P.dense != 0)) return;  // dense: k_mm_tma's sweep
     extern __shared__ __align__(16) unsigned char s_dyn[];
 #if TPA_MM5_SLIM
     // column states read straight from global memory and the CTA's

@@ -30,7 +30,6 @@
 #include "cpi_kernels.cuh"
 #include "cpi_spmm.cuh"
 #include "cpi_spmm5.cuh"
-#include "cpi_spmm_tma.cuh"
 #include "cpi_spmv2.cuh"
 #include "cpi_sweep1.cuh"
 #include "tpa_gpu.h"
@@ -463,8 +462,6 @@ struct Workspace {
     DevBuf limbs;                // partition mode: [3][6] fixed-point limbs (sweep parity 0/1, init) + [6] totals
     DevBuf sl;                   // sparse sweeps: segments of the marked long rows
     DevBuf dm_part;              // caller-supplied x: per-block signed dangling sums
-    bool has_tm = false;         // B = 32: tensor maps of share[0], share[1] for k_mm_tma
-    CUtensorMap tm[2];
 };
 
 // Long rows of CSR(Ãᵀ) (in-degree > kLong) cut into kLong-nnz segments, the
@@ -778,46 +775,6 @@ static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
 #endif
 }
 
-#ifndef TPA_MM_TMA
-#define TPA_MM_TMA 0
-#endif
-// Tensor maps of the B = 32 share ping-pong buffers ([n+1][32] f64, 256-byte
-// rows, box 32 x 1: one gather4 fetches four rows) for k_mm_tma.
-static void ensure_tensor_maps(tpa_graph* g, Workspace& w) {
-    if (w.has_tm) return;
-    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Encode enc = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<Encode>(fn);
-    }();
-    const cuuint64_t dims[2] = {(cuuint64_t)MmT::B, (cuuint64_t)g->n + 1};
-    const cuuint64_t strides[1] = {(cuuint64_t)MmT::B * 8};
-    const cuuint32_t box[2] = {(cuuint32_t)MmT::B, 1};
-    const cuuint32_t es[2] = {1, 1};
-    for (int k = 0; k < 2; ++k) {
-        const CUresult r = enc(&w.tm[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, w.share[k].p, dims, strides, box, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    }
-    w.has_tm = true;
-}
-
-template <bool L>
-static void launch_tma(const CUtensorMap& tm, const Mm4Args& P, int num_sms, cudaStream_t stream) {
-    static const bool ok = [] {
-        CK(cudaFuncSetAttribute(k_mm_tma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MmT::kDynSmem));
-        return true;
-    }();
-    (void)ok;
-    k_mm_tma<L><<<num_sms, MmT::NT, MmT::kDynSmem, stream>>>(tm, P);
-}
-
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
                         const SeedList* push_seeds = nullptr) {
     const Schedule& s = g->mv;
@@ -903,18 +860,6 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             g->launches -= 1;  // no pull this sweep: cancels the common ++ below
         } else {
             const bool last = a.out != nullptr;
-            if (TPA_MM_TMA && B == 32 && !g->part) {
-                // dense sweeps on the TMA gather kernel; K3 keeps the sparse ones
-                // (each kernel reads the device-side dense flag and leaves early
-                // when the sweep is the other's)
-                ensure_tensor_maps(g, w);
-                P.tma = 1;
-                const CUtensorMap& tm = w.tm[(a.step - 1) & 1];
-                if (last) launch_tma<true>(tm, P, g->num_sms, g->stream);
-                else launch_tma<false>(tm, P, g->num_sms, g->stream);
-                CKL("k_mm_tma");
-                g->launches += 1;
-            }
             if (B == 16) {
                 if (last) launch_fused_rb<16, true>(P, rb, g->num_sms, g->stream);
                 else launch_fused_rb<16, false>(P, rb, g->num_sms, g->stream);

@@ -1,5 +1,12 @@
-// cpi_spmm_tma.cuh -- K3t: the dense B = 32 sweep of a seed batch with the
-// share-row gathers on the Tensor Memory Accelerator (sm_100a tile::gather4).
+// cpi_spmm_tma.cuh -- EXPERIMENT (not built into the library): the dense
+// B = 32 sweep of a seed batch with the share-row gathers on the Tensor Memory
+// Accelerator (sm_100a tile::gather4).  Measured bitwise equal to K3 and 10x
+// slower (C4 sweep 4: 154 ms vs 14 ms): the single producer warp per SM walks
+// a dependent index -> frontier-bit -> issue chain per 32-position window
+// (~1.4 us each, 112 k windows per SM at C4); see profiles/r02_experiments.md.
+// It was wired into tpa_gpu.cu's launch_step for B = 32 (with a `tma` flag in
+// Mm4Args telling K3 to leave the dense sweeps) at commit "TMA gather4 SpMM
+// kernel k_mm_tma".
 //
 // K3 (cpi_spmm5.cuh) gathers every 256-byte share row with one LDG per lane
 // (lane = column): ~14 warp instructions per nonzero, 64 registers, 32 warps
