@@ -36,10 +36,8 @@ __global__ void __launch_bounds__(256) k_frontier_cost(const uint32_t* __restric
                                                        int B, unsigned long long limit) {
     const int lane = threadIdx.x & 31;
     // a Uniform spread reaches every row (graph.cpp:265-268): no sparse pull then
-#ifndef TPA_NO_SPREAD_GUARD  // (A/B only: reproduces the unguarded decision)
     if (blockIdx.x == 0 && (int)threadIdx.x < B && st[threadIdx.x].active && st[threadIdx.x].has_spread)
         atomicAdd(cost, 1ull << 62);
-#endif
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     unsigned long long c = 0;
     uint32_t k = 0;

@@ -41,14 +41,8 @@ constexpr int kThreads = 256;         // CTA size of every step kernel
 constexpr int kGroupItems = 128;      // items per first-level ticket group
 
 // SpMV (B = 1) tiling.
-#ifndef TPA_MV_TILE
-#define TPA_MV_TILE 2048
-#endif
-#ifndef TPA_MV_ROWS
-#define TPA_MV_ROWS 512
-#endif
-constexpr int kMvTileNnz = TPA_MV_TILE;  // gathered values staged in smem per CTA
-constexpr int kMvTileRows = TPA_MV_ROWS;
+constexpr int kMvTileNnz = 2048;  // largest SpMV tile (nnz); see mv_shape (cpi_spmv2.cuh)
+constexpr int kMvTileRows = 512;
 constexpr int kMvShortRow = 32;       // rows <= this: one thread, sequential
 
 // Per-column CPI state, double-buffered by sweep parity.
@@ -115,110 +109,13 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
     return r;
 }
 
-// ---- L2 residency (createpolicy + .L2::cache_hint) --------------------------
-// The sweeps gather the iterate at random while streaming everything else
-// (indices, row pointers, degrees, accumulators, outputs) once.  The streams
-// are marked evict_first so they do not displace the gathered iterate in the
-// 126 MB L2 (C4: 4.3 GB of acc / share / out traffic per B = 32 sweep).
-#ifndef TPA_HINT_STREAM
-#define TPA_HINT_STREAM 0
-#endif
-#ifndef TPA_HINT_GATHER  // iterate gathers: 0 evict_normal, 1 evict_last
-#define TPA_HINT_GATHER 0
-#endif
-#ifndef TPA_HINT_SHOUT  // next-iterate stores: 0 evict_normal, 1 evict_last, 2 evict_first
-#define TPA_HINT_SHOUT 0
-#endif
-struct L2Pol {
-    uint64_t first, last;
-};
-__device__ __forceinline__ L2Pol l2_policies() {
-    L2Pol p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.first));
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.last));
-    return p;
-}
-// read-once streams (never written by the kernel that reads them)
-__device__ __forceinline__ uint32_t ld_col(const uint32_t* p, const L2Pol& q) {
+// Loads of the sweeps' read-once streams and the gathered iterate.  (L2
+// eviction-priority hints on these were measured without gain and with extra
+// register pressure: profiles/r02_experiments.md.)
+__device__ __forceinline__ uint32_t ld_col(const uint32_t* p) {  // CSR indices: keep them out of L1
     uint32_t r;
-#if TPA_HINT_STREAM
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(q.first));
-#else
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-    (void)q;
-#endif
     return r;
-}
-__device__ __forceinline__ uint32_t ld_once_u32(const uint32_t* p, const L2Pol& q) {
-#if TPA_HINT_STREAM
-    uint32_t r;
-    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(q.first));
-    return r;
-#else
-    (void)q;
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ int64_t ld_once_s64(const int64_t* p, const L2Pol& q) {
-#if TPA_HINT_STREAM
-    int64_t r;
-    asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(q.first));
-    return r;
-#else
-    (void)q;
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double ld_once_f64(const double* p, const L2Pol& q) {
-#if TPA_HINT_STREAM
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(q.first));
-    return r;
-#else
-    (void)q;
-    return __ldg(p);
-#endif
-}
-// the window accumulator: read, then written back by the same thread
-__device__ __forceinline__ double ld_acc(const double* p, const L2Pol& q) {
-#if TPA_HINT_STREAM
-    double r;
-    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(q.first) : "memory");
-    return r;
-#else
-    (void)q;
-    return *p;
-#endif
-}
-__device__ __forceinline__ void st_stream(double* p, double v, const L2Pol& q) {
-#if TPA_HINT_STREAM
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(q.first) : "memory");
-#else
-    (void)q;
-    *p = v;
-#endif
-}
-// the next iterate (gathered by the next sweep)
-__device__ __forceinline__ void st_share(double* p, double v, const L2Pol& q) {
-#if TPA_HINT_SHOUT == 1
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(q.last) : "memory");
-#elif TPA_HINT_SHOUT == 2
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(q.first) : "memory");
-#else
-    (void)q;
-    *p = v;
-#endif
-}
-// one gathered iterate value (B = 1)
-__device__ __forceinline__ double ld_gather(const double* p, const L2Pol& q) {
-#if TPA_HINT_GATHER
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(q.last));
-    return r;
-#else
-    (void)q;
-    return __ldg(p);
-#endif
 }
 
 // Deterministic warp sum: xor butterfly, every lane ends with the same value.
@@ -358,15 +255,7 @@ template <> struct MmVec<64> { static constexpr int G = 32, CPL = 2; };
 
 // One lane's CPL columns of a gathered share row (B >= 8).
 template <int CPL>
-__device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL], const L2Pol& q) {
-#if TPA_HINT_GATHER
-    if constexpr (CPL == 1) {
-        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(q.last));
-    } else {
-        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(q.last));
-    }
-#else
-    (void)q;
+__device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
     if constexpr (CPL == 1) {
         v[0] = __ldg(p);
     } else {
@@ -374,7 +263,6 @@ __device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL], const
         v[0] = t.x;
         v[1] = t.y;
     }
-#endif
 }
 
 }  // namespace tpa

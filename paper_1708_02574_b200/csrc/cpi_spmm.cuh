@@ -36,16 +36,7 @@
 
 namespace tpa {
 
-#ifndef TPA_MM_ROWS
-#define TPA_MM_ROWS 16
-#endif
-#ifndef TPA_MM_MINB
-#define TPA_MM_MINB 1
-#endif
-#ifndef TPA_MM_DB
-#define TPA_MM_DB 1
-#endif
-constexpr int kMmRows = TPA_MM_ROWS;  // a block lies inside one aligned kMmRows-row window
+constexpr int kMmRows = 16;  // a block lies inside one aligned kMmRows-row window
 constexpr int kLong = 512;      // rows above: cut into kLong-nnz segments
 constexpr int kBlockNnz = 512;  // nnz cap of a block (bounds the longest work item)
 constexpr int kU = 8;           // stream chunk (positions); gathers per chunk = kU
@@ -274,7 +265,7 @@ __device__ __forceinline__ void consume_staged(const double* __restrict__ share,
             w[4 * q + 3] = t.w;
         }
 #pragma unroll
-        for (int j = 0; j < kU; ++j) ld_cols<CPL>(share + (size_t)w[j] * B + c0, v[j], l2_policies());
+        for (int j = 0; j < kU; ++j) ld_cols<CPL>(share + (size_t)w[j] * B + c0, v[j]);
     };
     auto consume = [&](int ci, const double (&v)[kU][CPL]) {
         const int base = ci * kU;
@@ -314,7 +305,7 @@ __device__ __forceinline__ void consume_staged(const double* __restrict__ share,
             }
         }
     };
-#if TPA_MM_DB
+    // double-buffered chunks: chunk ci+1's gathers are in flight while ci sums
     double va[kU][CPL], vb[kU][CPL];
     issue(0, va);
     for (int ci = 0; ci < nch; ci += 2) {
@@ -325,13 +316,6 @@ __device__ __forceinline__ void consume_staged(const double* __restrict__ share,
             consume(ci + 1, vb);
         }
     }
-#else
-    double va[kU][CPL];
-    for (int ci = 0; ci < nch; ++ci) {
-        issue(ci, va);
-        consume(ci, va);
-    }
-#endif
 }
 
 __device__ __forceinline__ double combine_value(const StepArgs& a, double f, uint32_t r) {
@@ -452,7 +436,7 @@ __device__ __forceinline__ void mm_epilogue_rows(const MmArgs& A, const ColState
 }
 
 template <int B>
-__global__ void __launch_bounds__(MmShape<B>::NT, (B == 32 ? TPA_MM_MINB : 1)) k_step_spmm2(MmArgs A) {
+__global__ void __launch_bounds__(MmShape<B>::NT, 1) k_step_spmm2(MmArgs A) {
     using Sh = MmShape<B>;
     constexpr int G = Sh::G, CPL = Sh::CPL, NGRP = Sh::NGRP, NT = Sh::NT;
     const StepArgs& a = A.s;

@@ -18,24 +18,6 @@
 
 namespace tpa {
 
-// A/B knobs: an unpredicated gather group when all its sources are live;
-// the window's gather groups unrolled (shuffle lanes become immediates).
-#ifndef TPA_MM5_ALL_LIVE
-#define TPA_MM5_ALL_LIVE 0
-#endif
-#ifndef TPA_MM5_UNROLL_H
-#define TPA_MM5_UNROLL_H 0
-#endif
-#ifndef TPA_MM5_TIMING_NO_LIVE
-#define TPA_MM5_TIMING_NO_LIVE 0
-#endif
-#ifndef TPA_MM5_SLIM
-#define TPA_MM5_SLIM 1  // B = 16: 1.018 -> 0.997 ms per C2 batch; B = 32 / 64 within noise
-#endif
-#ifndef TPA_MM5_MINB
-#define TPA_MM5_MINB 8
-#endif
-
 // B = 16 ("paired" form): a 128-byte share row is one half-warp's load, so
 // every gather instruction fetches TWO consecutive positions of the block's
 // nonzero stream (lanes 0-15 the even one, 16-31 the odd one), and a
@@ -62,41 +44,26 @@ struct Mm5 {
 };
 
 template <int CPL>
-__device__ __forceinline__ void cp_async_acc(double* dst_smem, const double* src, const L2Pol& q) {
+__device__ __forceinline__ void cp_async_acc(double* dst_smem, const double* src) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
-#if TPA_HINT_STREAM
-    if constexpr (CPL == 1)
-        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "l"(q.first)
-                     : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "l"(q.first)
-                     : "memory");
-#else
-    (void)q;
     if constexpr (CPL == 1)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-#endif
 }
 
 template <int B, bool kLast, int RB>
-__global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Args P) {
+__global__ void __launch_bounds__(Mm5<B, RB>::NT, 8) k_mm_fused(Mm4Args P) {
     using Sh = Mm5<B, RB>;
     constexpr int CPL = Sh::CPL, U = Sh::U, TS = Sh::TS;
     constexpr bool PAIR = Sh::PAIR;
     const MmArgs& A = P.m;
     const StepArgs& a = A.s;
     extern __shared__ __align__(16) unsigned char s_dyn[];
-#if TPA_MM5_SLIM
     // column states read straight from global memory and the CTA's
     // fixed-point totals aliased onto the (by then idle) dynamic tile:
     // 2 KB less static shared memory per CTA, left to the L1
     unsigned long long* s_fx = reinterpret_cast<unsigned long long*>(s_dyn);
-#else
-    __shared__ ColState s_st[B];
-    __shared__ unsigned long long s_fx[4 * B];
-#endif
     __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -105,24 +72,15 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     double (*yb)[B] = reinterpret_cast<double (*)[B]>(s_dyn + (size_t)wid * Sh::kWarpBytes);
     double* tile = reinterpret_cast<double*>(s_dyn + (size_t)wid * Sh::kWarpBytes + Sh::kYBytes);
 
-#if !TPA_MM5_SLIM
-    for (int i = tid; i < 4 * B; i += Sh::NT) s_fx[i] = 0ull;
-    for (int b = tid; b < B; b += Sh::NT) s_st[b] = a.state_in[b];
-#endif
     __syncthreads();
     ColState st[CPL];
     bool any_active = false;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-#if TPA_MM5_SLIM
         st[c] = a.state_in[c0 + c];
-#else
-        st[c] = s_st[c0 + c];
-#endif
         any_active = any_active || st[c].active;
     }
     any_active = __any_sync(0xffffffffu, any_active);
-    const L2Pol pol = l2_policies();
     const bool want_dm = a.policy == kUniform;
     unsigned long long fx[4][CPL];
 #pragma unroll
@@ -189,16 +147,16 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
             const int64_t hi = min(lo + (int64_t)kLong, (int64_t)__ldg(a.row_ptr + r0 + 1));
             rpl = lane == 0 ? lo : hi;
         } else {
-            rpl = lane <= nrows ? ld_once_s64(a.row_ptr + r0 + lane, pol) : 0;
+            rpl = lane <= nrows ? __ldg(a.row_ptr + r0 + lane) : 0;
         }
         // block epilogue inputs, fetched now so they land during the gathers
         const uint32_t av = (A.acc_valid && a.acc) ? __ldcg(A.acc_valid + (r0 >> 5)) : 0u;
-        const uint32_t dl = lane < nrows ? ld_once_u32(a.deg + r0 + lane, pol) : 0u;
+        const uint32_t dl = lane < nrows ? __ldg(a.deg + r0 + lane) : 0u;
         if (!is_seg && a.acc) {
             // PAIR: each half-warp fetches the rows its epilogue takes
             for (int k = PAIR ? half : 0; k < nrows; k += PAIR ? 2 : 1)
                 if ((av >> ((r0 + k) & 31)) & 1u)
-                    cp_async_acc<CPL>(tile + k * TS + c0, a.acc + (size_t)(r0 + k) * B + c0, pol);
+                    cp_async_acc<CPL>(tile + k * TS + c0, a.acc + (size_t)(r0 + k) * B + c0);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
 
@@ -230,15 +188,10 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
         // U-wide gather groups take their sources from the window by shuffle
         auto idx32 = [&](int64_t base) -> uint32_t {
             const int64_t e = base + lane;
-            return e < e1 ? ld_col(col + e, pol) : 0u;
+            return e < e1 ? ld_col(col + e) : 0u;
         };
         auto bits32 = [&](uint32_t u, int64_t base) -> uint32_t {
-#if TPA_MM5_TIMING_NO_LIVE  // TIMING PROBE ONLY (wrong results): no frontier lookups
-            (void)u; (void)base;
-            return 0xffffffffu;
-#else
             return (nz && base + lane < e1) ? __ldg(nz + (u >> 5)) : 0xffffffffu;
-#endif
         };
         if (any_active && e1 > e0) {
             uint32_t i0 = idx32(e0), i1 = idx32(e0 + 32);
@@ -248,11 +201,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 const uint32_t w1 = bits32(i1, wbase + 32);
                 const uint32_t live32 =
                     __ballot_sync(0xffffffffu, ((w0 >> (i0 & 31)) & 1u) && wbase + lane < e1);
-#if TPA_MM5_UNROLL_H
-#pragma unroll
-#else
 #pragma unroll 1
-#endif
                 for (int h = 0; h < 32 / U; ++h) {
                     const int64_t base = wbase + h * U;
                     if (base >= e1) break;  // warp-uniform
@@ -266,12 +215,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                         for (int jp = 0; jp < U / 2; ++jp) {
                             const int pp = 2 * jp + half;
                             const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + pp);
-                            v[jp] = 0.0;
-                            if ((lmask >> pp) & 1u) {
-                                double t1[1];
-                                ld_cols<1>(share + (size_t)u * B + c0, t1, pol);
-                                v[jp] = t1[0];
-                            }
+                            v[jp] = ((lmask >> pp) & 1u) ? __ldg(share + (size_t)u * B + c0) : 0.0;
                         }
                         // the term of position j: the lower half holds 2j'
                         // and receives 2j'+1 from the upper half, so its sum
@@ -309,24 +253,14 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                         }
                     } else if (!PAIR && lmask) {
                         double v[U][CPL];
-                        if (TPA_MM5_ALL_LIVE && lmask == (U == 32 ? 0xffffffffu : (1u << (U & 31)) - 1u)) {
-                            // every source of the group is live (dense sweeps): no
-                            // per-load predicates or zero fills
 #pragma unroll
-                            for (int j = 0; j < U; ++j) {
-                                const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
-                                ld_cols<CPL>(share + (size_t)u * B + c0, v[j], pol);
-                            }
-                        } else {
+                        for (int j = 0; j < U; ++j) {
+                            const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
+                            if ((lmask >> j) & 1u) {
+                                ld_cols<CPL>(share + (size_t)u * B + c0, v[j]);
+                            } else {
 #pragma unroll
-                            for (int j = 0; j < U; ++j) {
-                                const uint32_t u = __shfl_sync(0xffffffffu, i0, h * U + j);
-                                if ((lmask >> j) & 1u) {
-                                    ld_cols<CPL>(share + (size_t)u * B + c0, v[j], pol);
-                                } else {
-#pragma unroll
-                                    for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
-                                }
+                                for (int c = 0; c < CPL; ++c) v[j][c] = 0.0;
                             }
                         }
                         if (smask == 0) {
@@ -392,7 +326,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 yb[0][c0 + c] = y;
             }
             if (lane == 0) A.long_cnt[li] = 0;
-            if (a.acc && ((av >> (r0 & 31)) & 1u)) cp_async_acc<CPL>(tile + c0, a.acc + (size_t)r0 * B + c0, pol);
+            if (a.acc && ((av >> (r0 & 31)) & 1u)) cp_async_acc<CPL>(tile + c0, a.acc + (size_t)r0 * B + c0);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         } else if (ne_mask) {
 #pragma unroll
@@ -441,8 +375,8 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                     tile[k * TS + c0 + c] = combine_value(a, f, r);  // tpa.cpp:73-74
                 } else {
                     const double sh = d ? ddiv(dmul(a.keep, yy[c]), (double)d) : 0.0;  // graph.cpp:222
-                    st_stream(a.acc + ix, f, pol);
-                    st_share(a.share_out + ix, sh, pol);
+                    a.acc[ix] = f;
+                    a.share_out[ix] = sh;
                 }
                 bl1[c] = dadd(bl1[c], fabs(yy[c]));
                 if (want_dm && d == 0) bdm[c] = dadd(bdm[c], yy[c]);
@@ -465,7 +399,7 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
                 // transposed: RB lanes x 8 B contiguous of one seed's vector per store
                 const int k = lane % RB;
                 for (uint32_t b = lane / RB; b < a.b_valid; b += 32 / RB)
-                    if (k < nrows) st_stream(a.out + (size_t)b * a.n + r0 + k, tile[k * TS + b], pol);
+                    if (k < nrows) a.out[(size_t)b * a.n + r0 + k] = tile[k * TS + b];
             }
             __syncwarp();
         }
@@ -482,11 +416,9 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, TPA_MM5_MINB) k_mm_fused(Mm4Ar
     }
 
     // residual / dangling mass: exact integer sums; the last CTA advances state
-#if TPA_MM5_SLIM
     __syncthreads();  // every warp is done with its tile: s_fx may overlay it
     for (int i = tid; i < 4 * B; i += Sh::NT) s_fx[i] = 0ull;
     __syncthreads();
-#endif
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int b = c0 + c;

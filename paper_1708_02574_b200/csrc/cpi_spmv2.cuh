@@ -29,17 +29,14 @@ struct PeerOut {
     uint32_t n;
 };
 
-#ifndef TPA_MV2_SEGSCAN
-#define TPA_MV2_SEGSCAN 0
-#endif
-// values (TPA_MV2_SEGSCAN: padded by one double per 8), row pointers, row sums.
+// values, row pointers, row sums.
 // The size matters: 2 KB more per CTA cost 4% at C2 and 22% at C4 (less L1).
 // row offsets inside the tile (int32, relative to the tile's first nonzero)
 template <int kRows>
 __host__ __device__ constexpr size_t mv_rp_bytes() { return ((kRows + 1) * 4 + 7) / 8 * 8; }
 template <int kNnz, int kRows>
 __host__ __device__ constexpr size_t mv_dyn_smem() {
-    return ((size_t)kNnz + (TPA_MV2_SEGSCAN ? kNnz / 8 : 0)) * 8 + mv_rp_bytes<kRows>() + (size_t)kRows * 8;
+    return (size_t)kNnz * 8 + mv_rp_bytes<kRows>() + (size_t)kRows * 8;
 }
 constexpr size_t kMvDynSmem = mv_dyn_smem<kMvTileNnz, kMvTileRows>();
 
@@ -120,54 +117,38 @@ __device__ __forceinline__ double mv_block_sum(double v, double* s_red) {
     return r;
 }
 
-#ifndef TPA_MV2_PDL  // A/B: programmatic dependent launch between consecutive sweeps
-#define TPA_MV2_PDL 1  // C1 65.4 -> 68.3 GTEPS (launch-bound sweeps), C2 unchanged
-#endif
-#ifndef TPA_MV2_FX_SLOTS
-#define TPA_MV2_FX_SLOTS 1
-#endif
-constexpr int kMvFxSlots = TPA_MV2_FX_SLOTS;  // [4 x slots] fixed-point accumulators (w.fx, B = 1)
-#ifndef TPA_MV2_EARLY_EXIT  // 1: 0.1102 -> 0.1097 ms per C2 sweep, 3.232 -> 3.220 at C4
-#define TPA_MV2_EARLY_EXIT 1
-#endif
-#ifdef TPA_MV2_MINB  // A/B knob; the default (no minimum) compiles to 40 registers, 6 CTAs/SM
-template <bool kRanked, int kThr, int kNnz, int kRows>
-__global__ void __launch_bounds__(kThr, TPA_MV2_MINB) k_step_spmv2(MvArgs M) {
-#else
+constexpr int kMvFxSlots = 1;  // [4 x slots] fixed-point accumulators (w.fx, B = 1)
+// Consecutive sweeps are chained by programmatic dependent launch (C1 65.4 ->
+// 68.3 GTEPS: launch-bound sweeps); only thread 0 of a finished CTA takes the
+// ticket (0.1102 -> 0.1097 ms per C2 sweep).  The default register
+// allocation (40, no minimum-blocks bound) measured best.
 template <bool kRanked, int kThr, int kNnz, int kRows>
 __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
-#endif
     const StepArgs& a = M.s;
     // the tile's staging in dynamic shared memory (kMvDynSmem bytes): values,
     // row pointers, row sums
     extern __shared__ __align__(16) unsigned char s_mv[];
     double* s_vals = reinterpret_cast<double*>(s_mv);
-    int* s_rp = reinterpret_cast<int*>(s_vals + kNnz + (TPA_MV2_SEGSCAN ? kNnz / 8 : 0));  // row starts - nb
+    int* s_rp = reinterpret_cast<int*>(s_vals + kNnz);  // row starts - nb
     double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + mv_rp_bytes<kRows>());
     __shared__ double s_red[kThr / 32];
-    __shared__ uint32_t s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t item = blockIdx.x;
     // tile totals spread over kMvFxSlots accumulator pairs: fewer same-address
     // atomics serialising in one L2 slice (the last CTA adds the slots)
     const int fx_slot = (int)(item % kMvFxSlots);
-#if TPA_MV2_PDL
     // programmatic dependent launch: the next sweep's CTAs may start once
     // every CTA of this one has; they wait below for this grid to finish
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
     const uint2 it = a.items[item];  // the tiling is static: read before the wait
     const uint32_t rb = it.x, re = it.y & ~kLongFlag;
     const bool is_long = (it.y & kLongFlag) != 0;
     const longlong2 nr = M.item_nnz[item];
     const int64_t nb = nr.x, ne = nr.y;
-#if TPA_MV2_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous sweep's shares, acc, state
-#endif
     const ColState st = a.state_in[0];
-    const L2Pol pol = l2_policies();
-
+    
     if (!st.active) {
         // column stopped earlier: only a pending combine remains (tpa.cpp:73)
         if (a.out)
@@ -196,130 +177,26 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int k = tid + j * kThr;
-            u[j] = k < nnz ? ld_col(a.col + nb + k, pol) : 0u;
+            u[j] = k < nnz ? ld_col(a.col + nb + k) : 0u;
         }
-        for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(ld_once_s64(a.row_ptr + rb + r, pol) - nb);
+        for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(__ldg(a.row_ptr + rb + r) - nb);
         uint32_t dg[RPT], so[RPT];
         double ac[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const uint32_t r = tid + q * kThr;
-            dg[q] = r < nrows ? ld_once_u32(a.deg + rb + r, pol) : 0u;
-            if constexpr (kRanked) so[q] = r < nrows ? ld_once_u32(a.rank + rb + r, pol) : 0u;  // share slot
+            dg[q] = r < nrows ? __ldg(a.deg + rb + r) : 0u;
+            if constexpr (kRanked) so[q] = r < nrows ? __ldg(a.rank + rb + r) : 0u;  // share slot
             else so[q] = rb + r;
-            ac[q] = (r < nrows && a.acc) ? ld_acc(a.acc + rb + r, pol) : 0.0;
+            ac[q] = (r < nrows && a.acc) ? a.acc[rb + r] : 0.0;
         }
         // ---- round trip 2: gathers ----
         double v[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int k = tid + j * kThr;
-            v[j] = k < nnz ? ld_gather(a.share_in + u[j], pol) : 0.0;
+            v[j] = k < nnz ? __ldg(a.share_in + u[j]) : 0.0;
         }
-#if TPA_MV2_SEGSCAN
-        // (A/B experiment, measured slower: C2 0.126-0.139 ms vs 0.110, C4
-        // 3.54-4.25 vs 3.22; 48-62 registers)
-        // nnz-balanced row sums: thread t owns positions [8t, 8t + 8) of the
-        // tile; a segmented scan (in-thread sequential, then a fixed
-        // shuffle / warp tree across threads) carries rows that span
-        // threads.  Every thread does the same work whatever the row lengths,
-        // so no thread idles at the barrier behind a long row.  The order is
-        // a function of the tile (identical in a row partition, which cuts at
-        // tile starts).  s_vals is padded (one double per 8) so the blocked
-        // reads below are bank-conflict free.
-        static_assert(kNnz == 8 * kThr, "segmented sums assume 8 nnz per thread");
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const int k = tid + j * kThr;
-            if (k < nnz) s_vals[k + (k >> 3)] = v[j];
-        }
-        for (uint32_t r = tid; r < nrows; r += kThr) s_y[r] = 0.0;  // empty rows stay 0
-        __syncthreads();
-        {
-            const int p0 = tid * 8;
-            // the row holding position p0: the last r with s_rp[r] <= p0
-            int r = 0;
-            if (p0 < nnz) {
-                int lo = 0, hi = (int)nrows - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_rp[mid] <= p0) lo = mid;
-                    else hi = mid - 1;
-                }
-                r = lo;
-            }
-            const int r_first = r;
-            int next = p0 < nnz ? s_rp[r + 1] : 0;  // end of row r
-            double x[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = p0 + i < nnz ? s_vals[p0 + i + (p0 >> 3)] : 0.0;
-            // pass 1: the thread's aggregate (sum since its last row start)
-            uint32_t starts = 0;  // bit i: position p0 + i starts a row
-            {
-                int rr = r, nx = next;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = p0 + i;
-                    if (k < nnz && k == nx) {
-                        starts |= 1u << i;
-                        while (s_rp[rr + 1] <= k) ++rr;
-                        nx = s_rp[rr + 1];
-                    }
-                }
-            }
-            if (p0 < nnz && s_rp[r] == p0) starts |= 1u;
-            double agg = 0.0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) agg = ((starts >> i) & 1u) ? x[i] : dadd(agg, x[i]);
-            int aflag = starts != 0;
-            // exclusive segmented scan of (agg, aflag) over the CTA
-            double iv = agg;
-            int ifl = aflag;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double pv = __shfl_up_sync(0xffffffffu, iv, o);
-                const int pf = __shfl_up_sync(0xffffffffu, ifl, o);
-                if (lane >= o && !ifl) iv = dadd(pv, iv);
-                if (lane >= o) ifl |= pf;
-            }
-            __shared__ double s_wv[kThr / 32];
-            __shared__ int s_wf[kThr / 32];
-            if (lane == 31) {
-                s_wv[warp] = iv;
-                s_wf[warp] = ifl;
-            }
-            __syncthreads();
-            double cv = 0.0;  // carry from the warps before this one
-            int cf = 0;
-            for (int w = 0; w < warp; ++w) {
-                cv = s_wf[w] ? s_wv[w] : dadd(cv, s_wv[w]);
-                cf |= s_wf[w];
-            }
-            double ev = __shfl_up_sync(0xffffffffu, iv, 1);  // exclusive within the warp
-            int ef = __shfl_up_sync(0xffffffffu, ifl, 1);
-            if (lane == 0) {
-                ev = 0.0;
-                ef = 0;
-            }
-            const double carry = ef ? ev : dadd(cv, ev);
-            (void)cf;
-            // pass 2: running sums; a row's value is final at its last position
-            double run = carry;
-            int rr = r_first, nx = next;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = p0 + i;
-                if (k >= nnz) break;
-                run = ((starts >> i) & 1u) ? x[i] : dadd(run, x[i]);
-                if (k == nx - 1) {
-                    s_y[rr] = run;
-                    // on to the row holding position k + 1 (past empty rows)
-                    while (rr + 1 < (int)nrows && s_rp[rr + 1] <= k + 1) ++rr;
-                    nx = s_rp[rr + 1];
-                }
-            }
-        }
-#else
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int k = tid + j * kThr;
@@ -351,7 +228,6 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
                 if (lane == 0) s_y[rr] = s;
             }
         }
-#endif
         __syncthreads();
         // epilogue with the prefetched degree / accumulator of each row
 #pragma unroll
@@ -365,15 +241,14 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             if (a.acc) {
                 const double f = dadd(ac[q], y);  // cpi.cpp:50
                 if (a.out) {
-                    st_stream(a.out + vtx, a.stranger ? dadd(dmul(a.scale, f), ld_once_f64(a.stranger + vtx, pol))
-                                                      : dmul(f, a.scale), pol);
+                    a.out[vtx] = a.stranger ? dadd(dmul(a.scale, f), a.stranger[vtx]) : dmul(f, a.scale);
                 } else {
-                    st_stream(a.acc + vtx, f, pol);
+                    a.acc[vtx] = f;
                 }
             }
             if (a.share_out) {
                 const double sv = dg[q] ? ddiv(dmul(a.keep, y), (double)dg[q]) : 0.0;
-                st_share(a.share_out + so[q], sv, pol);
+                a.share_out[so[q]] = sv;
                 for (uint32_t k = 0; k < M.peers.n; ++k) M.peers.p[k][vtx] = sv;
             }
             add_row(y, dg[q] == 0);
@@ -387,13 +262,13 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             uint32_t u[U];
             double v[U];
 #pragma unroll
-            for (int j = 0; j < U; ++j) u[j] = ld_col(a.col + e + j * kThr, pol);
+            for (int j = 0; j < U; ++j) u[j] = ld_col(a.col + e + j * kThr);
 #pragma unroll
-            for (int j = 0; j < U; ++j) v[j] = ld_gather(a.share_in + u[j], pol);
+            for (int j = 0; j < U; ++j) v[j] = __ldg(a.share_in + u[j]);
 #pragma unroll
             for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
         }
-        for (; e < ne; e += kThr) s = dadd(s, ld_gather(a.share_in + ld_col(a.col + e, pol), pol));
+        for (; e < ne; e += kThr) s = dadd(s, __ldg(a.share_in + ld_col(a.col + e)));
         s = mv_block_sum<kThr>(s, s_red);
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
@@ -430,21 +305,11 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             }
         }
     }
-#if TPA_MV2_EARLY_EXIT
     // only thread 0 takes the ticket: the rest of the CTA leaves now instead
     // of waiting out the fence + atomic round trip
-    (void)s_ticket;
     if (tid != 0) return;
     __threadfence();
     if (atomicAdd(a.done_cnt, 1u) != gridDim.x - 1) return;
-#else
-    if (tid == 0) {
-        __threadfence();
-        s_ticket = atomicAdd(a.done_cnt, 1u);
-    }
-    __syncthreads();
-    if (s_ticket != gridDim.x - 1 || tid != 0) return;
-#endif
     __threadfence();
     // exact 128-bit sums of the slots (order-free)
     unsigned long long h0 = 0, l0 = 0, h1 = 0, l1 = 0;

@@ -139,9 +139,6 @@ struct DevBuf {
 // nodes ordered by out-degree, descending (ties by id).  The hot sources --
 // C4: the top 10% of nodes feed 89% of the gathers -- then share 32-byte
 // sectors and L2 lines instead of being spread over the whole vector.
-#ifndef TPA_RANKED
-#define TPA_RANKED 1
-#endif
 __global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint32_t n, uint32_t* __restrict__ keys,
                             uint32_t* __restrict__ ids) {
     for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
@@ -758,7 +755,6 @@ static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
         return true;
     }();
     (void)ok;
-#if TPA_MV2_PDL
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THR);
@@ -769,10 +765,7 @@ static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, k_step_spmv2<RF, THR, NNZ, ROWS>, M));
-#else
-    k_step_spmv2<RF, THR, NNZ, ROWS><<<grid, THR, smem, stream>>>(M);
-#endif
+    CK(cudaLaunchKernelEx(&cfg, k_step_spmv2<RF, THR, NNZ, ROWS>, M));  // programmatic dependent launch
 }
 
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
@@ -1377,7 +1370,7 @@ int tpa_graph_create(uint32_t n, uint64_t m, const uint64_t* out_offsets,
         // the L2 (C4: 134 MB, C5: 2.1 GB), if the column copy fits comfortably
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
-        if (TPA_RANKED && m && (uint64_t)n * 8 > (64ull << 20) && m * 4 + (uint64_t)n * 24 < free_b / 2) {
+        if (m && (uint64_t)n * 8 > (64ull << 20) && m * 4 + (uint64_t)n * 24 < free_b / 2) {
             DevBuf keys, keys2, ids, perm, tmp;
             keys.ensure((size_t)n * 4, s);
             keys2.ensure((size_t)n * 4, s);
