@@ -123,6 +123,15 @@ def test_config_full(cfg, oracle):
     assert_close(pr3.scores, w[0], what=f"{cfg} pagerank window [0,3]")
     assert pr3.iterations_run == w[1] == 3
 
+    # the row-partitioned run (unranked partition CSRs, tpa_part.cuh) is bitwise the
+    # whole-graph one (C4: the ranked share layout) -- the same additions in the same order
+    if cfg == "c4":
+        grp = P.PartitionGroup(g, [0, 0])
+        try:
+            assert np.array_equal(grp.preprocess(C, EPS, T), st), "partitioned C4 preprocess differs"
+        finally:
+            grp.close()
+
     # every query of the bench job: closed-form mass
     nsf = P.neighbor_scale_factor(C, S, T)
     mass = (1 + nsf) * (1 - (1 - C) ** S) + float(st.sum())

@@ -12,6 +12,7 @@
 // argv[1] = rows of X (default 2^20: 268 MB, partly L2-resident; 16777216 is
 // C4's 4.3 GB share matrix)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_micro tools/gather_micro.cu
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cuda.h>
@@ -237,6 +238,36 @@ int main(int argc, char** argv) {
         char nm[64];
         snprintf(nm, 64, "LDG U=16, %d warps/SM", warps);
         timeit(nm, [&] { gather_ldg<16><<<sms * warps / 8, 256>>>(X, idx, m, out); });
+    }
+    {
+        // L2 persistence: the hot rows (the first n/64, half of all gathers) in a
+        // persisting access-policy window, the rest streaming
+        int maxp = 0;
+        CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0));
+        const size_t hot = (size_t)(n / 64) * B * 8;
+        printf("max persisting L2 %d bytes; hot region %zu bytes\n", maxp, hot);
+        for (double frac : {0.5, 1.0}) {
+            const size_t win = std::min<size_t>(hot, (size_t)maxp);
+            CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)(maxp * frac)));
+            cudaStreamAttrValue av{};
+            av.accessPolicyWindow.base_ptr = X;
+            av.accessPolicyWindow.num_bytes = win;
+            av.accessPolicyWindow.hitRatio = 1.0f;
+            av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStream_t st;
+            CK(cudaStreamCreate(&st));  // blocking: orders with the timing events on the legacy stream
+            CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+            for (int warps : {32, 48}) {
+                char nm[80];
+                snprintf(nm, 80, "LDG U=16 %dw persist %.0f%%", warps, frac * 100);
+                timeit(nm, [&] { gather_ldg<16><<<sms * warps / 8, 256, 0, st>>>(X, idx, m, out); });
+            }
+            av.accessPolicyWindow.num_bytes = 0;
+            CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av));
+            CK(cudaStreamDestroy(st));
+            CK(cudaCtxResetPersistingL2Cache());
+        }
     }
     auto ring = [&](auto kern, int S, int R, int wpb) {
         const size_t smem = (size_t)wpb * S * R * B * 8;
