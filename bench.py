@@ -555,11 +555,13 @@ def run_ours(args):
     Bk = batch if batch > 1 else 1
     if batch > 1 and mm_cnt:
         # dominant kernel: the SpMM sweep.  Roofline on its densest launch, the
-        # last family sweep x^(S-1) (fused combine), with that sweep's exact
-        # compulsory bytes; the sparse early sweeps are listed per index.
+        # last family sweep x^(S-1) (fused combine); the sparse early sweeps are
+        # listed per index.
         kname = f"k_mm_fused<{Bk}>" if Bk >= 16 else f"k_step_spmm2<{Bk}>"
         last = per_sweep.get(S - 1)
-        bytes_launch = sweep_bytes(n, m, Bk, "last")
+        # SURVEY §8(d)'s per-sweep figure A_step(B, acc=1) (what the roofline is
+        # defined on); the engine's own compulsory count is reported beside it
+        bytes_launch = a_step(n, m, Bk, 1)
         avg_ms = last["avg_ms"] if last else mm_ms / mm_cnt
         share = mm_ms / prof_total_ms if prof_total_ms else None
     else:
@@ -581,20 +583,29 @@ def run_ours(args):
                 "traffic": traffic_per_launch(kname, cfg_name), "algorithmic_bytes_per_launch": bytes_launch,
                 "avg_launch_ms": avg_ms, "launches_timed": mm_cnt if batch > 1 else mv_cnt,
                 "share_of_step": share, "per_sweep": per_sweep,
-                "survey_a_step_bytes": a_step(n, m, Bk, 1),
+                "bytes_definition": "SURVEY 8(d) A_step(B,1) = 4m + 8(n+1) + 8n + 32Bn per sweep",
+                "engine_compulsory_bytes": sweep_bytes(n, m, Bk, "last") if batch > 1 else a_step(n, m, 1, 1),
                 "spmv": {"launches": mv_cnt, "avg_ms": mv_ms / max(mv_cnt, 1),
                          "achieved_gbs": a_step(n, m, 1, 1) / (mv_ms / max(mv_cnt, 1) / 1e3) / 1e9
                          if mv_cnt else None}}
-    if batch > 1 and mb.get("gather_256B_rows"):
+    # the measured ceiling of the access pattern at this working-set size: the
+    # L2-resident one, or the one measured at C4's size once the iterate is far
+    # beyond the 126 MB L2
+    big = n * Bk * 8 > (1 << 30)
+    key_mm = "gather_256B_rows_4GB" if big else "gather_256B_rows"
+    if batch > 1 and mb.get(key_mm):
         g_gbs = m * Bk * 8 / (avg_ms / 1e3) / 1e9  # every nonzero gathers one B-wide share row
-        pk = mb["gather_256B_rows"]["best_gbs"] if Bk == 32 else None
+        pk = mb[key_mm]["best_gbs"] if Bk == 32 else None
         roofline["gather_bound"] = {"achieved_gbs": g_gbs, "peak_gbs": pk, "frac": g_gbs / pk if pk else None,
+                                    "pattern": mb[key_mm]["pattern"],
                                     "source": "profiles/microbench.json (tools/gather_micro.cu)"}
-    if mv_cnt and mb.get("gather_8B"):
+    key_mv = "gather_8B_134MB" if n * 8 > (64 << 20) else "gather_8B"
+    if mv_cnt and mb.get(key_mv):
         rate = m / (mv_ms / mv_cnt / 1e3)
         roofline["spmv"]["gather_bound"] = {"achieved_gathers_per_s": rate,
-                                            "peak_gathers_per_s": mb["gather_8B"]["best_gathers_per_s"],
-                                            "frac": rate / mb["gather_8B"]["best_gathers_per_s"]}
+                                            "peak_gathers_per_s": mb[key_mv]["best_gathers_per_s"],
+                                            "frac": rate / mb[key_mv]["best_gathers_per_s"],
+                                            "pattern": mb[key_mv]["pattern"]}
 
     # end-to-end through the public API with host buffers
     # The e2e legs run with the process on the GPU's own NUMA node, so the
