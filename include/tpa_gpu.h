@@ -247,6 +247,17 @@ int tpa_group_cpi_run(tpa_group *grp, const uint32_t *seeds, uint64_t n_seeds, d
                       uint32_t *iterations_run, int *converged, double *residual_l1);
 /* preprocess's stranger vector (window [T, inf)); out: n doubles. */
 int tpa_group_preprocess(tpa_group *grp, double c, double eps, uint32_t T, double *out_stranger);
+/* query / query_na for B seeds on the row-partitioned graph (graphs beyond one
+ * GPU): tpa_query_batch's semantics and errors (tpa.cpp:61-86) with the
+ * artifact given by its fields -- stranger (n doubles, host or device via UVA;
+ * unused with TPA_QUERY_NA), the graph fingerprint it was built for, c, eps, T.
+ * The B-seed sweep runs on every partition's rows of the padded share layout;
+ * spans, frontier words and exact residual limbs are exchanged per sweep
+ * (peer copies).  out: [B][n] seed-major, host, or device with
+ * TPA_DEVICE_PTRS.  Up to 16 partitions.  Scores equal the whole-graph
+ * tpa_query_batch bit for bit under SelfLoop / Drop (Uniform: within rounding). */
+int tpa_group_query_batch(tpa_group *grp, const double *stranger, uint64_t fingerprint, double c, double eps,
+                          uint32_t T, const uint32_t *seeds, uint32_t B, uint32_t S, double *out, int flags);
 
 /* --- host-side graph plumbing (not on the hot path) -----------------------
  * A host graph with the reference Graph's construction semantics

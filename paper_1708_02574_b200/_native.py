@@ -72,6 +72,7 @@ SIGNATURES = {
     "tpa_group_cpi_run": ([_vp, _vp, _u64, _dbl, _dbl, _u32, _i64, _vp, C.POINTER(_u32), C.POINTER(_int),
                            C.POINTER(_dbl)], _int),
     "tpa_group_preprocess": ([_vp, _dbl, _dbl, _u32, _vp], _int),
+    "tpa_group_query_batch": ([_vp, _vp, _u64, _dbl, _dbl, _u32, _vp, _u32, _u32, _vp, _int], _int),
     "tpa_host_graph_from_edges": ([_u32, _vp, _vp, _u64, _int, C.POINTER(_vp)], _int),
     "tpa_host_graph_build_gpu": ([_u32, _vp, _vp, _u64, _int, _int, C.POINTER(_vp)], _int),
     "tpa_host_graph_rmat_gpu": ([_u32, _u32, _dbl, _dbl, _dbl, _u64, _int, _int, C.POINTER(_vp)], _int),

@@ -61,6 +61,9 @@ struct MmArgs {
     // scheduling / reduction
     uint32_t* work_cnt;       // zero between launches
     unsigned long long* fx;   // [4B]: l1 hi/lo, dm hi/lo per column; zero between launches
+    // row partition (tpa_part.cuh): the last CTA publishes the sweep's exact
+    // totals as limbs [B][6] here and leaves the state to k_part_finalize_b
+    unsigned long long* limbs_out;
 };
 
 // ---- 128-bit fixed point (value = hi*2^-56 + lo*2^-120), for y in [0, 2^7) --
@@ -89,6 +92,22 @@ __device__ __forceinline__ double seg_sum(const double* p, size_t stride, uint32
     }
     for (; j < ns; ++j) y = dadd(y, __ldcg(p + (size_t)j * stride));
     return y;
+}
+
+// 128-bit fixed-point totals as three limbs each (hi, lo >> 32, lo & 2^32-1):
+// limb-wise integer sums over up to 2^31 partitions cannot overflow, and
+// limbs_to_fx restores the exact 128-bit total (NCCL all-reduce of uint64).
+__device__ __forceinline__ void fx_to_limbs(unsigned long long hi, unsigned long long lo, unsigned long long* L) {
+    L[0] = hi;
+    L[1] = lo >> 32;
+    L[2] = lo & 0xffffffffull;
+}
+__device__ __forceinline__ void limbs_to_fx(const unsigned long long* L, unsigned long long& hi,
+                                            unsigned long long& lo) {
+    const unsigned long long t2 = L[2];
+    const unsigned long long t1 = L[1] + (t2 >> 32);
+    lo = ((t1 & 0xffffffffull) << 32) | (t2 & 0xffffffffull);
+    hi = L[0] + (t1 >> 32);
 }
 
 __device__ __forceinline__ double fx_decode(unsigned long long hi, unsigned long long lo) {

@@ -440,6 +440,12 @@ __global__ void __launch_bounds__(Mm5<B, RB>::NT, 8) k_mm_fused(Mm4Args P) {
         ColState sc = a.state_in[b];
         const unsigned long long h0 = atomicAdd(&A.fx[4 * b + 0], 0ull), l0 = atomicAdd(&A.fx[4 * b + 1], 0ull);
         const unsigned long long h1 = atomicAdd(&A.fx[4 * b + 2], 0ull), l1 = atomicAdd(&A.fx[4 * b + 3], 0ull);
+        if (A.limbs_out) {  // a partition's totals: summed over partitions by k_part_finalize_b
+            fx_to_limbs(h0, l0, A.limbs_out + 6 * b);
+            fx_to_limbs(h1, l1, A.limbs_out + 6 * b + 3);
+            A.fx[4 * b + 0] = A.fx[4 * b + 1] = A.fx[4 * b + 2] = A.fx[4 * b + 3] = 0ull;
+            continue;
+        }
         if (sc.active) {
             const double res = fx_decode(h0, l0);
             const double dm = fx_decode(h1, l1);

@@ -68,22 +68,6 @@ struct MvArgs {
     uint32_t limb_off;                       // limbs - share_out, in doubles (peer copies of the limbs)
 };
 
-// 128-bit fixed-point totals as three limbs each (hi, lo >> 32, lo & 2^32-1):
-// limb-wise integer sums over up to 2^31 partitions cannot overflow, and
-// limbs_to_fx restores the exact 128-bit total (NCCL all-reduce of uint64).
-__device__ __forceinline__ void fx_to_limbs(unsigned long long hi, unsigned long long lo, unsigned long long* L) {
-    L[0] = hi;
-    L[1] = lo >> 32;
-    L[2] = lo & 0xffffffffull;
-}
-__device__ __forceinline__ void limbs_to_fx(const unsigned long long* L, unsigned long long& hi,
-                                            unsigned long long& lo) {
-    const unsigned long long t2 = L[2];
-    const unsigned long long t1 = L[1] + (t2 >> 32);
-    lo = ((t1 & 0xffffffffull) << 32) | (t2 & 0xffffffffull);
-    hi = L[0] + (t1 >> 32);
-}
-
 // ColState after sweep `step` from the global residual / dangling mass
 // (cpi.cpp:73-80; Uniform spread graph.cpp:265-268).
 __device__ __forceinline__ ColState advance_state(ColState s, double res, double dmt, const StepArgs& a) {

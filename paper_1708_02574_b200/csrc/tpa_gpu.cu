@@ -596,14 +596,15 @@ struct tpa_graph {
         // B > 1: one extra all-zero row (index n) that dead sources gather
         const size_t nb = (size_t)n * B * sizeof(double);
         // a partition's shares span the padded global layout (all partitions)
-        const size_t nbs = part ? (size_t)part->nranks * part->stride * sizeof(double)
-                                : nb + (B > 1 ? (size_t)B * sizeof(double) : 0);
+        // (the padded rows of every partition, then for B > 1 the zero row)
+        const size_t rows_sh = part ? (size_t)part->nranks * part->stride : (size_t)n;
+        const size_t nbs = rows_sh * B * sizeof(double) + (B > 1 ? (size_t)B * sizeof(double) : 0);
         if (w.share[0].bytes < nbs) {
             w.share[0].ensure(nbs, stream);
             w.share[1].ensure(nbs, stream);
             if (B > 1) {
-                CK(cudaMemsetAsync(w.share[0].as<double>() + (size_t)n * B, 0, (size_t)B * 8, stream));
-                CK(cudaMemsetAsync(w.share[1].as<double>() + (size_t)n * B, 0, (size_t)B * 8, stream));
+                CK(cudaMemsetAsync(w.share[0].as<double>() + rows_sh * B, 0, (size_t)B * 8, stream));
+                CK(cudaMemsetAsync(w.share[1].as<double>() + rows_sh * B, 0, (size_t)B * 8, stream));
             }
         }
         w.acc.ensure(nb, stream);
@@ -624,7 +625,7 @@ struct tpa_graph {
             CK(cudaMemsetAsync(w.long_cnt.p, 0, w.long_cnt.bytes, stream));
         }
         if (B > 1 && !w.work_cnt.p) {
-            const size_t words = ((size_t)n + 31) / 32 + 1;
+            const size_t words = (rows_sh + 31) / 32 + 1;  // frontier bitmaps span the share rows
             w.nz[0].ensure(words * 4, stream);
             w.nz[1].ensure(words * 4, stream);
             w.acc_valid.ensure(words * 4, stream);
@@ -809,7 +810,7 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
             }
             CKL("k_s1_push");
             g->launches += 2;  // k_s1_rows + k_s1_push (the common ++ below is cancelled)
-        } else if (mm->nz_in && a.step <= kSparseSweeps) {
+        } else if (mm->nz_in && a.step <= kSparseSweeps && !g->part) {
             const uint32_t words = (g->n + 31) / 32;
             auto* ctl = w.sparse_ctl.as<unsigned long long>();
             CK(cudaMemsetAsync(w.sparse_ctl.p, 0, 32, g->stream));
@@ -1041,7 +1042,7 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             // sweep 1 of a seed batch: a push from the seeds (one term per
             // element) instead of a pull over every nonzero
             const bool s1 = mm && i == 1 && cfg.init == Init::Seeds && a.acc && a.share_out && !a.out &&
-                            !cfg.y_out && g->policy != kUniform && B >= 16;
+                            !cfg.y_out && g->policy != kUniform && B >= 16 && !g->part;
             launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr);
         }
         done += chunk;

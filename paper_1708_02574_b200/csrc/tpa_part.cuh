@@ -186,7 +186,7 @@ static void build_part(tpa_graph* g, uint32_t n, uint64_t m, const uint64_t* out
     uint32_t S = 1;
     for (uint32_t r = 0; r < nranks; ++r) S = std::max(S, P->rows(r));
     P->slice = S;
-    P->stride = S + kLimbPad;
+    P->stride = (S + kLimbPad + 31) / 32 * 32;  // word-aligned spans in the B > 1 frontier bitmaps
     const uint32_t lo = P->bounds[rank], hi = P->bounds[rank + 1], nl = hi - lo;
     const uint64_t ml = prefix[hi] - prefix[lo];
 
@@ -598,6 +598,7 @@ static void run_cpi_part(std::vector<tpa_graph*>& Pg, PartRun& cfg) {
 
 struct tpa_group {
     std::vector<tpa_graph*> parts;
+    std::vector<uint32_t> gdeg;  // global out-degrees (seed shares of query batches)
     std::mutex mu;
 };
 
@@ -648,6 +649,275 @@ static void part_preprocess(std::vector<tpa_graph*>& Pg, double c, double eps, u
     cfg.terminal = -1;
     cfg.out = out;
     run_cpi_part(Pg, cfg);
+}
+
+// ---- row-partitioned query batches (B = 16 / 32 / 64) ------------------------
+// The B-seed sweep K3 over the partitions: each partition pulls its rows from
+// the padded global share layout [G*stride rows + a zero row][B], stores its
+// rows' next shares (and frontier bits) into its own span, and publishes its
+// exact residual totals as limbs; the spans and limbs are exchanged per sweep
+// and k_part_finalize_b advances the same column states everywhere.  The rows'
+// arithmetic is K3's, so the scores equal the whole-graph query_batch bit for
+// bit (SelfLoop / Drop; a Uniform spread comes from per-block dangling sums,
+// which a partition groups differently: equal within rounding).  tpa.cpp:61-86.
+struct SeedShares {
+    double v[64];
+};
+
+// node id -> row of the padded global share layout (owner r: the last
+// partition starting at or before v, skipping empty ones; as k_part_keys)
+struct PartMap {
+    uint32_t bounds[kMaxPeerOut + 2];
+    uint32_t G, stride;
+    static PartMap of(const PartInfo& P) {
+        PartMap m{};
+        m.G = P.nranks;
+        m.stride = P.stride;
+        for (uint32_t r = 0; r <= P.nranks; ++r) m.bounds[r] = P.bounds[r];
+        return m;
+    }
+    __device__ uint32_t padded(uint32_t v) const {
+        uint32_t a = 0, b = G;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (bounds[mid] <= v) a = mid;
+            else b = mid;
+        }
+        return a * stride + (v - bounds[a]);
+    }
+};
+
+// x⁰ of the batch: every partition writes every seed's share row at its owner's
+// padded position (the whole x⁰ is known on the host: no exchange needed), the
+// frontier bit, and -- for the seeds it owns -- the accumulator row.
+__global__ void k_init_seeds_part(const SeedList seeds, SeedShares sh, uint32_t b_valid, int B, double c,
+                                  PartMap pm, uint32_t lo, uint32_t hi, double* __restrict__ share0,
+                                  double* __restrict__ acc0, uint32_t* __restrict__ nz0,
+                                  uint32_t* __restrict__ acc_valid) {
+    const int b = threadIdx.x;
+    if (b >= (int)b_valid) return;
+    const uint32_t seed = seeds.s[b];
+    const uint32_t pr = pm.padded(seed);
+    for (int k = 0; k < B; ++k) {
+        const bool mine = k < (int)b_valid && seeds.s[k] == seed;
+        share0[(size_t)pr * B + k] = mine ? sh.v[k] : 0.0;
+        if (seed >= lo && seed < hi) acc0[(size_t)(seed - lo) * B + k] = mine ? c : 0.0;
+    }
+    atomicOr(nz0 + (pr >> 5), 1u << (pr & 31));
+    if (seed >= lo && seed < hi) atomicOr(acc_valid + ((seed - lo) >> 5), 1u << ((seed - lo) & 31));
+}
+
+struct LimbSets {
+    const unsigned long long* p[kMaxPeerOut + 1];
+};
+
+// The per-column states after a partitioned sweep: the exact sum of every
+// partition's limbs, then K3's update (cpi.cpp:73-80).
+__global__ void k_part_finalize_b(LimbSets L, uint32_t G, int B, StepArgs a) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    unsigned long long t[6] = {0, 0, 0, 0, 0, 0};
+    for (uint32_t r = 0; r < G; ++r)
+        for (int k = 0; k < 6; ++k) t[k] += L.p[r][6 * b + k];
+    unsigned long long h0, l0, h1, l1;
+    limbs_to_fx(t, h0, l0);
+    limbs_to_fx(t + 3, h1, l1);
+    ColState sc = a.state_in[b];
+    if (sc.active) {
+        const double res = fx_decode(h0, l0), dm = fx_decode(h1, l1);
+        sc.residual = res;
+        sc.iters = a.step;
+        sc.converged = res < a.eps;
+        sc.active = !sc.converged && (a.terminal < 0 || (int64_t)a.step < a.terminal);
+        sc.has_spread = (a.policy == kUniform && dm != 0.0);
+        sc.spread = sc.has_spread ? ddiv(dmul(a.keep, dm), (double)a.n) : 0.0;
+    }
+    a.state_out[b] = sc;
+}
+
+// One query batch over the in-process partitions Pg (all of one graph).
+// stranger: n doubles (host or device, UVA), null for query_na; out: [Btot][n]
+// seed-major on the device of Pg[0] (dev) or the host.
+static void run_batch_part(std::vector<tpa_graph*>& Pg, const std::vector<uint32_t>& gdeg, const uint32_t* seeds,
+                           uint32_t Btot, double c, double eps, uint32_t S, const double* stranger, double scale,
+                           double* out, bool dev) {
+    const uint32_t G = Pg[0]->part->nranks;
+    if (Pg.size() != G) throw std::invalid_argument("a partitioned query batch needs every partition");
+    if (G > (uint32_t)kMaxPeerOut + 1) throw std::invalid_argument("a partitioned query batch takes <= 16 partitions");
+    const uint32_t n = Pg[0]->part->n_global;
+    const double keep = 1.0 - c;
+    for (uint32_t b = 0; b < Btot; ++b) validate_seed(seeds[b], n);
+    // per partition: the stranger slice and (host output) a device staging buffer
+    std::vector<DevBuf> str(G), limbs(G);
+    DevBuf stage;
+    double* out_dev = out;
+    {
+        DeviceGuard dg(Pg[0]->device);
+        if (!dev) {
+            stage.ensure((size_t)std::min<uint32_t>(Btot, 64) * n * 8, Pg[0]->stream);
+            out_dev = stage.as<double>();
+        }
+    }
+    for (uint32_t k = 0; k < G; ++k) {
+        tpa_graph* g = Pg[k];
+        DeviceGuard dg(g->device);
+        limbs[k].ensure(64 * 6 * 8, g->stream);
+        if (stranger && g->n) {
+            str[k].ensure((size_t)g->n * 8, g->stream);
+            CK(cudaMemcpyAsync(str[k].p, stranger + g->part->row_begin(), (size_t)g->n * 8, cudaMemcpyDefault,
+                               g->stream));
+        }
+    }
+    const int64_t terminal = (int64_t)S - 1;
+    for (uint32_t b0 = 0; b0 < Btot; b0 += 64) {
+        const uint32_t bv = std::min<uint32_t>(64, Btot - b0);
+        const int B = std::max(16, batch_width(bv));
+        SeedList sl{};
+        SeedShares sh{};
+        std::vector<ColState> st0(B);
+        for (uint32_t b = 0; b < bv; ++b) {
+            const uint32_t sd = seeds[b0 + b];
+            sl.s[b] = sd;
+            const uint32_t d = gdeg[sd];
+            sh.v[b] = d ? (keep * c) / (double)d : 0.0;  // graph.cpp:222 (host IEEE double, no FMA)
+            ColState& s = st0[b];
+            s.iters = 0;
+            s.converged = 0;
+            s.residual = c;
+            s.active = terminal != 0;
+            s.has_spread = Pg[0]->policy == kUniform && d == 0;
+            s.spread = s.has_spread ? (keep * c) / (double)n : 0.0;
+        }
+        for (int b = (int)bv; b < B; ++b) st0[b] = ColState{};
+        double* out_b = dev ? out + (size_t)b0 * n : out_dev;
+        std::vector<StepArgs> A(G);
+        std::vector<MmArgs> M(G);
+        for (uint32_t k = 0; k < G; ++k) {
+            tpa_graph* g = Pg[k];
+            DeviceGuard dg(g->device);
+            Workspace& w = g->workspace(B);
+            const PartInfo& P = *g->part;
+            const size_t rows_sh = (size_t)G * P.stride;
+            const size_t bm = (rows_sh + 31) / 32 * 4 + 4;
+            CK(cudaMemsetAsync(w.nz[0].p, 0, bm, g->stream));
+            CK(cudaMemsetAsync(w.acc_valid.p, 0, ((size_t)g->n + 31) / 32 * 4 + 4, g->stream));
+            CK(cudaMemcpyAsync(w.state.p, st0.data(), B * sizeof(ColState), cudaMemcpyHostToDevice, g->stream));
+            k_init_seeds_part<<<1, 64, 0, g->stream>>>(sl, sh, bv, B, c, PartMap::of(P), P.row_begin(),
+                                                       P.row_begin() + g->n, w.share[0].as<double>(),
+                                                       w.acc.as<double>(), w.nz[0].as<uint32_t>(),
+                                                       w.acc_valid.as<uint32_t>());
+            CKL("k_init_seeds_part");
+            ++g->launches;
+            StepArgs& a = A[k];
+            a = StepArgs{};
+            a.row_ptr = g->row_ptr.as<int64_t>();
+            a.col = g->col.as<uint32_t>();
+            a.deg = g->deg.as<uint32_t>();
+            a.n = n;  // the graph's n: Uniform spread, and the seed-major output's row length
+            a.policy = g->policy;
+            a.keep = keep;
+            a.eps = eps;
+            a.terminal = terminal;
+            a.scale = scale;
+            a.b_valid = bv;
+            a.stranger = stranger ? str[k].as<double>() : nullptr;
+            a.acc = w.acc.as<double>();
+            a.done_cnt = w.done_cnt.as<uint32_t>();
+            MmArgs& ma = M[k];
+            ma = MmArgs{};
+            ma.seg_row = g->longs.seg_row.as<uint32_t>();
+            ma.seg_lo = g->longs.seg_lo.as<int64_t>();
+            ma.seg_long = g->longs.seg_long.as<uint32_t>();
+            ma.long_first = g->longs.long_first.as<uint32_t>();
+            ma.long_nseg = g->longs.long_nseg.as<uint32_t>();
+            ma.long_cnt = w.long_cnt.as<uint32_t>();
+            ma.seg_part = w.seg_part.as<double>();
+            ma.n_segs = g->longs.n_segs;
+            ma.n_blocks = g->n_blocks;
+            ma.blocks = g->longs.blocks.as<uint2>();
+            ma.zero_row = (uint32_t)rows_sh;
+            ma.work_cnt = w.work_cnt.as<uint32_t>();
+            ma.fx = w.fx.as<unsigned long long>();
+            ma.acc_valid = w.acc_valid.as<uint32_t>();
+            ma.limbs_out = limbs[k].as<unsigned long long>();
+        }
+        for (int64_t i = 1; i <= terminal; ++i) {
+            const bool last = i == terminal;
+            for (uint32_t k = 0; k < G; ++k) {
+                tpa_graph* g = Pg[k];
+                DeviceGuard dg(g->device);
+                Workspace& w = g->workspace(B);
+                const PartInfo& P = *g->part;
+                const size_t bm = ((size_t)G * P.stride + 31) / 32 * 4 + 4;
+                StepArgs& a = A[k];
+                ColState* st = w.state.as<ColState>();
+                a.step = (uint32_t)i;
+                a.share_in = w.share[(i - 1) & 1].as<double>();
+                a.share_out = last ? nullptr : w.share[i & 1].as<double>() + (size_t)P.rank * P.stride * B;
+                a.out = last ? out_b + P.row_begin() : nullptr;
+                a.state_in = st + ((i - 1) & 1) * B;
+                a.state_out = st + (i & 1) * B;
+                MmArgs& ma = M[k];
+                ma.s = a;
+                ma.nz_in = w.nz[(i - 1) & 1].as<uint32_t>();
+                ma.nz_out = last ? nullptr : w.nz[i & 1].as<uint32_t>() + P.rank * P.stride / 32;
+                if (!last) CK(cudaMemsetAsync(w.nz[i & 1].p, 0, bm, g->stream));
+                if (g->n) {
+                    launch_step(g, w, a, &ma, B);
+                } else {  // an empty partition contributes nothing
+                    CK(cudaMemsetAsync(limbs[k].p, 0, (size_t)B * 6 * 8, g->stream));
+                }
+            }
+            // exchange: every partition's span (shares + frontier words) and limbs
+            std::vector<cudaEvent_t> ev(G);
+            for (uint32_t r = 0; r < G; ++r) {
+                DeviceGuard dg(Pg[r]->device);
+                ev[r] = Pg[r]->take_event();
+                CK(cudaEventRecord(ev[r], Pg[r]->stream));
+            }
+            LimbSets ls{};
+            for (uint32_t r = 0; r < G; ++r) ls.p[r] = limbs[r].as<unsigned long long>();
+            for (uint32_t q = 0; q < G; ++q) {
+                tpa_graph* g = Pg[q];
+                DeviceGuard dg(g->device);
+                for (uint32_t r = 0; r < G; ++r) CK(cudaStreamWaitEvent(g->stream, ev[r], 0));
+                Workspace& w = g->workspace(B);
+                if (!last) {
+                    for (uint32_t r = 0; r < G; ++r) {
+                        if (r == q) continue;
+                        const PartInfo& Pr = *Pg[r]->part;
+                        const uint32_t rows = Pr.rows(r);
+                        if (!rows) continue;
+                        Workspace& wr = Pg[r]->workspace(B);
+                        const size_t row0 = (size_t)r * Pr.stride;
+                        CK(cudaMemcpyPeerAsync(w.share[i & 1].as<double>() + row0 * B, g->device,
+                                               wr.share[i & 1].as<double>() + row0 * B, Pg[r]->device,
+                                               (size_t)rows * B * 8, g->stream));
+                        CK(cudaMemcpyPeerAsync(w.nz[i & 1].as<uint32_t>() + row0 / 32, g->device,
+                                               wr.nz[i & 1].as<uint32_t>() + row0 / 32, Pg[r]->device,
+                                               ((size_t)rows + 31) / 32 * 4, g->stream));
+                    }
+                }
+                StepArgs& a = A[q];
+                k_part_finalize_b<<<1, 64, 0, g->stream>>>(ls, G, B, a);
+                CKL("k_part_finalize_b");
+                ++g->launches;
+            }
+            for (uint32_t r = 0; r < G; ++r) Pg[r]->event_pool.push_back(ev[r]);
+        }
+        if (!dev) {
+            for (uint32_t k = 0; k < G; ++k) {
+                DeviceGuard dg(Pg[k]->device);
+                CK(cudaStreamSynchronize(Pg[k]->stream));
+            }
+            DeviceGuard dg(Pg[0]->device);
+            CK(cudaMemcpy(out + (size_t)b0 * n, out_dev, (size_t)bv * n * 8, cudaMemcpyDeviceToHost));
+        }
+    }
+    for (tpa_graph* g : Pg) {
+        DeviceGuard dg(g->device);
+        CK(cudaStreamSynchronize(g->stream));
+    }
 }
 
 }  // namespace tpa
@@ -832,6 +1102,8 @@ int tpa_group_create(uint32_t n, uint64_t m, const uint64_t* out_offsets, const 
         if (nparts == 0 || nparts > 64) throw std::invalid_argument("a group has 1..64 partitions");
         if (!devices) throw std::invalid_argument("null device list");
         auto grp = std::make_unique<tpa_group>();
+        grp->gdeg.resize(n);
+        for (uint32_t u = 0; u < n; ++u) grp->gdeg[u] = (uint32_t)(out_offsets[u + 1] - out_offsets[u]);
         try {
             for (uint32_t r = 0; r < nparts; ++r)
                 grp->parts.push_back(
@@ -880,6 +1152,30 @@ int tpa_group_cpi_run(tpa_group* grp, const uint32_t* seeds, uint64_t n_seeds, d
         std::lock_guard<std::mutex> lk(grp->mu);
         part_cpi_run(grp->parts, seeds, n_seeds, c, eps, start_iter, terminal_iter, out_scores, iterations_run,
                      converged, residual_l1);
+    });
+}
+
+int tpa_group_query_batch(tpa_group* grp, const double* stranger, uint64_t fingerprint, double c, double eps,
+                          uint32_t T, const uint32_t* seeds, uint32_t B, uint32_t S, double* out, int flags) {
+    return guard([&] {
+        if (!grp) throw std::invalid_argument("null group");
+        std::lock_guard<std::mutex> lk(grp->mu);
+        tpa_graph* g0 = grp->parts[0];
+        const bool na = flags & TPA_QUERY_NA;
+        // tpa.cpp:63-66 (query) / tpa.cpp:8-17 (query_na's TpaParams::validate)
+        if (!na && fingerprint != g0->fingerprint)
+            throw std::runtime_error("stale artifact: graph fingerprint mismatch");
+        if (!na && (S < 1 || S >= T)) throw std::invalid_argument("family_end (S) must satisfy 1 <= S < T");
+        if (na && S < 1) throw std::invalid_argument("family_end (S) must be at least 1");
+        if (na && T <= S) throw std::invalid_argument("stranger_start (T) must exceed family_end (S)");
+        validate_cpi(c, eps, 0, (int64_t)S - 1);
+        if (!na && !stranger) throw std::invalid_argument("null stranger vector");
+        if (flags & TPA_NODE_MAJOR) throw std::invalid_argument("a partitioned batch writes seed-major output");
+        if (B == 0) return;
+        if (!seeds || !out) throw std::invalid_argument("null seeds or output");
+        const double scale = 1.0 + tpa_neighbor_scale_factor(c, S, T);
+        run_batch_part(grp->parts, grp->gdeg, seeds, B, c, eps, S, na ? nullptr : stranger, scale, out,
+                       (flags & TPA_DEVICE_PTRS) != 0);
     });
 }
 

@@ -21,7 +21,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 from ._native import check, lib
-from .graph import Graph
+from . import _native as N
+from .graph import Graph, vec_ptr
 from .tpa import CpiParams, CpiResult, SeedSet, _terminal
 
 COMM_ID_BYTES = 128
@@ -249,6 +250,31 @@ class PartitionGroup:
     def preprocess(self, c: float, eps: float, stranger_start: int) -> np.ndarray:
         out = np.empty(self.n, np.float64)
         check(lib.tpa_group_preprocess(self.h, float(c), float(eps), int(stranger_start), out.ctypes.data))
+        return out
+
+    def query_batch(self, artifact, seeds, family_end: int, out=None, na: bool = False, params=None):
+        """query / query_na (tpa.cpp:61-86) for a batch of seeds on the partitioned
+        graph; ``artifact`` is a StrangerArtifact (ignored with ``na``, which takes
+        ``params`` = TpaParams).  Returns [B][n] (numpy, or fills a CUDA tensor)."""
+        from .tpa import _seed_array
+        s = _seed_array(seeds, self.n)
+        B = int(s.size)
+        if out is None:
+            out = np.empty((B, self.n), np.float64)
+        p, dev, keep = vec_ptr(out, B * self.n, writable=True)
+        flags = (N.TPA_DEVICE_PTRS if dev else 0) | (N.TPA_QUERY_NA if na else 0)
+        if na:
+            prm = params
+            check(lib.tpa_group_query_batch(self.h, None, 0, float(prm.restart_prob), float(prm.tolerance),
+                                            int(prm.stranger_start), s.ctypes.data, B, int(family_end), p, flags))
+        else:
+            st = np.ascontiguousarray(artifact.stranger_scores, np.float64)
+            if st.size != self.n:
+                raise ValueError("stranger vector length does not match node count")
+            check(lib.tpa_group_query_batch(self.h, st.ctypes.data, int(artifact.graph_fingerprint),
+                                            float(artifact.restart_prob), float(artifact.tolerance),
+                                            int(artifact.stranger_start), s.ctypes.data, B, int(family_end), p,
+                                            flags))
         return out
 
     def close(self):
