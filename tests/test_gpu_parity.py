@@ -390,6 +390,14 @@ def test_c2_config_full(oracle):
             for k in (0, 31):
                 assert_close(host[k], oracle.query(g, want, c, eps, T, int(seeds[b0 + k]), S),
                              what=f"C2 query {b0 + k}")
+        if b0 == 512:
+            # one whole batch element-wise (32 oracle queries on the host cores)
+            from concurrent.futures import ThreadPoolExecutor
+            host = out.cpu().numpy()
+            with ThreadPoolExecutor(8) as ex:
+                ws = list(ex.map(lambda k: oracle.query(g, want, c, eps, T, int(seeds[b0 + k]), S), range(32)))
+            for k in range(32):
+                assert_close(host[k], ws[k], what=f"C2 query {b0 + k}")
 
 
 @pytest.mark.gpu
