@@ -903,6 +903,9 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
 // convergence (terminal < 0) checks the state on the host after the
 // estimated horizon, and continues if a column is still active.
 
+#ifndef TPA_MV_PERSIST
+#define TPA_MV_PERSIST 0
+#endif
 static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int B = cfg.B;
     Workspace& w = g->workspace(B);
@@ -919,6 +922,18 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const uint32_t* const deg_run = g->deg.as<uint32_t>();
     // B = 1 over the ranked share layout when the graph has one (rows unchanged)
     const uint32_t* const rank = (B == 1 && !partition && g->rank.p) ? g->rank.as<uint32_t>() : nullptr;
+    // ranked B = 1 sweeps: the hottest shares (the first slots) in a persisting L2 window
+    size_t persist = 0;
+    if (TPA_MV_PERSIST && rank) {
+        static const size_t maxp = [] {
+            int dev = 0, v = 0;
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev));
+            if (v > 0) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v));
+            return (size_t)std::max(v, 0);
+        }();
+        persist = std::min<size_t>(maxp, (size_t)n * 8);
+    }
 
     // accumulator for x⁽⁰⁾, zero the rest
     double* acc0 = nullptr;
@@ -1043,6 +1058,15 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             // element) instead of a pull over every nonzero
             const bool s1 = mm && i == 1 && cfg.init == Init::Seeds && a.acc && a.share_out && !a.out &&
                             !cfg.y_out && g->policy != kUniform && B >= 16 && !g->part;
+            if (persist) {  // the hot (lowest-rank) shares of this sweep's input persist in L2
+                cudaStreamAttrValue av{};
+                av.accessPolicyWindow.base_ptr = const_cast<double*>(a.share_in);
+                av.accessPolicyWindow.num_bytes = persist;
+                av.accessPolicyWindow.hitRatio = 1.0f;
+                av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+            }
             launch_step(g, w, a, mm ? &ma : nullptr, B, s1 ? &cfg.seeds : nullptr);
         }
         done += chunk;
@@ -1062,6 +1086,12 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
             cfg.node_major ? 1 : 0, cfg.out);
         CKL("k_combine");
         ++g->launches;
+    }
+    if (persist) {
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.num_bytes = 0;
+        CK(cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+        CK(cudaCtxResetPersistingL2Cache());
     }
     if (res && cfg.want_state) {
         res->state.resize(B);
