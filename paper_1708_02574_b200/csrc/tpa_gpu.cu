@@ -903,9 +903,6 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
 // convergence (terminal < 0) checks the state on the host after the
 // estimated horizon, and continues if a column is still active.
 
-#ifndef TPA_MV_PERSIST
-#define TPA_MV_PERSIST 0
-#endif
 static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const int B = cfg.B;
     Workspace& w = g->workspace(B);
@@ -922,9 +919,11 @@ static void run_cpi(tpa_graph* g, RunCfg& cfg, RunOut* res) {
     const uint32_t* const deg_run = g->deg.as<uint32_t>();
     // B = 1 over the ranked share layout when the graph has one (rows unchanged)
     const uint32_t* const rank = (B == 1 && !partition && g->rank.p) ? g->rank.as<uint32_t>() : nullptr;
-    // ranked B = 1 sweeps: the hottest shares (the first slots) in a persisting L2 window
+    // ranked B = 1 sweeps over a share vector far beyond the L2 (C5: 2.1 GB): the
+    // hottest shares (the first slots) in a persisting L2 window -- C5's DRAM-bound
+    // PageRank sweep 36.4 -> 34.9 ms; none at C4 (134 MB: LSU-bound), so not used there
     size_t persist = 0;
-    if (TPA_MV_PERSIST && rank) {
+    if (rank && (size_t)n * 8 > (1ull << 30)) {
         static const size_t maxp = [] {
             int dev = 0, v = 0;
             CK(cudaGetDevice(&dev));
