@@ -375,10 +375,26 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TPA_BENCH_SAME_DEVICE=1 (tests only): every rank on cuda:0 with a gloo
+    # group -- walks the N > 1 code path (partition, IPC exchange, barriers, the
+    # max-over-ranks reduce, the JSON line) on a one-GPU box; never a measurement
+    same_device = world > 1 and os.environ.get("TPA_BENCH_SAME_DEVICE") == "1"
+    if same_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t_ = torch.tensor([x], dtype=torch.float64, device="cpu" if same_device else dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
 
     cfg_name = args.config
     _, _, nq, batch, seed = CONFIGS[cfg_name]
@@ -536,10 +552,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     total_ms = sum(times)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
 
     # sweeps actually run: 116 PageRank sweeps (the convergence break) + (S-1) per query
@@ -647,13 +660,11 @@ def run_ours(args):
             el.append(time.perf_counter() - t0)
             lib.tpa_artifact_destroy(art)
             h2d, d2h = h2d_s, d2h_s
-        tt = torch.tensor([sum(el)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": edges_per_step * jobs * e2e_steps / float(tt.item()) / 1e9, "unit": "GTEPS",
+        e2e_s = max_over_ranks(sum(el))
+        e2e = {"value": edges_per_step * jobs * e2e_steps / e2e_s / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "queries_per_s": nq * jobs * e2e_steps / float(tt.item()),
-               "steps": e2e_steps, "ms_per_step": float(tt.item()) / e2e_steps * 1e3,
+               "queries_per_s": nq * jobs * e2e_steps / e2e_s,
+               "steps": e2e_steps, "ms_per_step": e2e_s / e2e_steps * 1e3,
                "note": "C-ABI with host buffers: seeds from host, stranger + every full score vector "
                        "copied back to pinned host memory (the reference API returns ScoreVectors); "
                        "batch calls with TPA_ASYNC: batch k+1 computes while batch k drains over PCIe"}
@@ -684,13 +695,11 @@ def run_ours(args):
             if it:
                 el.append(time.perf_counter() - t0)
             lib.tpa_artifact_destroy(art)
-        tt = torch.tensor([sum(el)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_topk = {"value": edges_per_step * jobs * len(el) / float(tt.item()) / 1e9, "unit": "GTEPS",
+        e2e_s = max_over_ranks(sum(el))
+        e2e_topk = {"value": edges_per_step * jobs * len(el) / e2e_s / 1e9, "unit": "GTEPS",
                     "k": K, "h2d_bytes_per_step": len(seeds) * 4, "d2h_bytes_per_step": len(seeds) * K * 12,
-                    "queries_per_s": nq * jobs * len(el) / float(tt.item()),
-                    "ms_per_step": float(tt.item()) / len(el) * 1e3,
+                    "queries_per_s": nq * jobs * len(el) / e2e_s,
+                    "ms_per_step": e2e_s / len(el) * 1e3,
                     "note": "tpa_query_batch_topk: query batch + device top_k_nodes (metrics.cpp:25-36); "
                             "ids and scores of the top 10 per seed to pinned host memory"}
 
@@ -711,6 +720,17 @@ def run_ours(args):
         del rg
 
     if rank == 0:
+        clocks = clk.summary()
+        gb = roofline.get("gather_bound")
+        if gb and clocks.get("sm_mhz"):
+            # a pull SpMM moves m x B x 8 bytes from L2 to the SMs whatever the hit
+            # rate: the L2 slices' aggregate cap (B300_MICROARCH.md "LTS throughput
+            # cap", ~6,300 B/clk, same L2 design) at the clock sustained in the run
+            l2_peak = 6300.0 * clocks["sm_mhz"] * 1e6 / 1e9
+            roofline["l2_bound"] = {"achieved_gbs": gb["achieved_gbs"], "peak_gbs": l2_peak,
+                                    "frac": gb["achieved_gbs"] / l2_peak,
+                                    "peak_source": "6,300 B/clk (microarchitecture notes, B300-measured) x "
+                                                   "median SM clock of this run"}
         line = {
             "metric": "CPI edges/sec (GTEPS) and online RWR queries/sec; % of HBM roofline",
             "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -720,7 +740,7 @@ def run_ours(args):
             "queries_per_s": qps, "preprocess_sweeps": pre_sweeps,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e if e2e is not None else e2e_topk,
             "e2e_topk": e2e_topk, "gpu_launches": launches,
-            "clocks": clk.summary(), "ingest_s": t_ingest, "graph_build_s": t_build,
+            "clocks": clocks, "ingest_s": t_ingest, "graph_build_s": t_build,
             "e2e_host_cpus": sorted(local_cpus) if local_cpus else "all",
             "outputs": ("per batch: the B full score vectors written to HBM (the idle iterate buffer), then the "
                         "device top-10 per seed kept resident (tpa_query_batch_topk)" if resident_topk else

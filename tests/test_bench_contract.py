@@ -46,6 +46,30 @@ def test_gpu_arm_line():
     assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["clocks"]["samples"] > 0
 
 
+@pytest.mark.gpu
+def test_two_rank_launch_walks_the_partitioned_path():
+    """The driver's N > 1 launch line with two ranks, both on cuda:0
+    (TPA_BENCH_SAME_DEVICE=1: gloo group, the product's CUDA IPC exchange
+    between the two processes).  Not a measurement: it checks that the
+    multi-rank path runs end to end and prints rank 0's single line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, TPA_BENCH_SAME_DEVICE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "c2", "--steps", "2", "--warmup", "3", "--no-cpu"],
+                       capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert KEYS <= set(d), KEYS - set(d)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert "ipc" in d["parallelism"] and d["preprocess_sweeps"] == 116
+
+
 def test_reference_arm_imports_no_product_code():
     """--impl reference must time the reference alone: nothing of the product
     package (nor its libtpa_gpu.so) is loaded in that process."""
