@@ -106,6 +106,50 @@ __global__ void gather(const double* __restrict__ X, const uint32_t* __restrict_
     if (s == 12345.678) out[0] = s;
 }
 
+// E: UL LDG gathers + UB 16-byte bulk copies per lane and iteration: does the
+// TMA engine's request path add to the LSU's?
+template <int UL, int UB>
+__global__ void gather_mixed(const double* __restrict__ X, const uint32_t* __restrict__ idx, long long m, double* out) {
+    __shared__ __align__(16) double sm[8][UB][64];
+    __shared__ uint64_t bar[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) mbar_init(&bar[w], 1);
+    __syncwarp();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    constexpr int U = UL + UB;
+    double s = 0.0;
+    uint32_t phase = 0;
+    for (long long base = warp * U * 32; base < m; base += nw * U * 32) {
+        uint32_t u[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const long long e = base + j * 32 + lane;
+            u[j] = e < m ? __ldcs(idx + e) : 0u;
+        }
+        if (lane == 0) mbar_expect_tx(&bar[w], UB * 32 * 16);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < UB; ++j) {
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(&sm[w][j][2 * lane]);
+            asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(d),
+                         "l"(X + (u[UL + j] & ~1u)), "r"((uint32_t)__cvta_generic_to_shared(&bar[w])) : "memory");
+        }
+        double v[UL];
+#pragma unroll
+        for (int j = 0; j < UL; ++j) v[j] = __ldg(X + u[j]);
+#pragma unroll
+        for (int j = 0; j < UL; ++j) s += v[j];
+        mbar_wait(&bar[w], phase);
+#pragma unroll
+        for (int j = 0; j < UB; ++j) s += sm[w][j][2 * lane + (u[UL + j] & 1)];
+        phase ^= 1;
+        __syncwarp();
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
 int main(int argc, char** argv) {
     const uint32_t n = argc > 1 ? (uint32_t)atoll(argv[1]) : (1u << 20);
     const long long m = 16586831;
@@ -159,6 +203,15 @@ int main(int argc, char** argv) {
         timeit(nm, [&] { gather_bulk16<8><<<sms * warps / 8, 256>>>(X, idx, m, out); });
         snprintf(nm, 64, "BULK16 U=4 %d w/SM", warps);
         timeit(nm, [&] { gather_bulk16<4><<<sms * warps / 8, 256>>>(X, idx, m, out); });
+    }
+    for (int warps : {32, 48, 64}) {
+        char nm[64];
+        snprintf(nm, 64, "MIXED LDG 14 + BULK 2 %d w/SM", warps);
+        timeit(nm, [&] { gather_mixed<14, 2><<<sms * warps / 8, 256>>>(X, idx, m, out); });
+        snprintf(nm, 64, "MIXED LDG 12 + BULK 4 %d w/SM", warps);
+        timeit(nm, [&] { gather_mixed<12, 4><<<sms * warps / 8, 256>>>(X, idx, m, out); });
+        snprintf(nm, 64, "MIXED LDG 6 + BULK 2 %d w/SM", warps);
+        timeit(nm, [&] { gather_mixed<6, 2><<<sms * warps / 8, 256>>>(X, idx, m, out); });
     }
     return 0;
 }
