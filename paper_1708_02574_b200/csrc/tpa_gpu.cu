@@ -544,7 +544,6 @@ struct tpa_graph {
     uint32_t n_blocks = 0;  // kMmRows-row blocks
     std::map<int, std::unique_ptr<Workspace>> ws;
     DevBuf init_part;
-    DevBuf out_stage;  // (unused; kept for the handle layout of older callers)
     // host-output pipeline of batch calls: chunk k computes into stage[k % 2] on
     // `stream` while chunk k-1's results drain to the host on `copy`
     struct HostPipe {
@@ -1460,7 +1459,6 @@ int tpa_graph_destroy(tpa_graph* g) {
                 d->release();
             g->init_part.release();
             for (DevBuf* d : {&g->topk.st, &g->topk.hist, &g->topk.cand, &g->topk.ids}) d->release();
-            g->out_stage.release();
             if (g->pipe.copy) {
                 cudaStreamSynchronize(g->pipe.copy);
                 for (int k = 0; k < 2; ++k) {

@@ -1,3 +1,9 @@
+// EXPERIMENT, not part of libtpa_gpu.so (profiles/r02_experiments.md, "Pipelined K2").
+// A drop-in replacement for csrc/cpi_spmv2.cuh in which one CTA takes up to 16
+// consecutive tiles and software-pipelines them; it needs MvArgs::per_cta set by
+// the launcher (mv_items_per_cta) and grid = ceil(n_items / per_cta).  Bitwise
+// K2, measured slower (96 registers, 5 CTAs/SM).
+//
 // cpi_spmv2.cuh -- K2 v2: the B = 1 sweep (PageRank / single-vector CPI).
 //
 // Same tiles and the same per-row arithmetic order as K2 v1 (cpi_kernels.cuh:

@@ -1,3 +1,8 @@
+// EXPERIMENT, not part of libtpa_gpu.so (profiles/r02_experiments.md, "K2h").
+// Include after csrc/cpi_spmv2.cuh; launch one CTA per SM with
+// mvh_dyn_smem<...>() bytes of dynamic shared memory over the ranked layout.
+// Bitwise K2, measured slower or equal at every hub size.
+//
 // cpi_spmv_hub.cuh -- K2h: the B = 1 sweep over the ranked share layout with
 // the hub slice of the share vector staged in shared memory.
 //
