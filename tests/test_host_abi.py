@@ -178,3 +178,16 @@ def test_vec_ptr_rejects_bad_buffers():
     assert p == a.ctypes.data and not dev and keep is a
     p, dev, keep = vec_ptr([1, 2, 3], 3)  # inputs may be converted
     assert keep.dtype == np.float64
+
+
+def test_compute_entry_points_fail_loudly_without_a_gpu():
+    """No CPU fallback: on a box without a CUDA device every compute entry
+    raises the library's CUDA error instead of returning numbers."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    g = P.generate_rmat(8, 8, rng_seed=3)
+    with pytest.raises(P.CudaError):
+        P.preprocess(g, 0.15, 1e-9, 10)
+    with pytest.raises(P.CudaError):
+        P.pagerank(g, P.CpiParams(0.15, 1e-9))
