@@ -140,3 +140,33 @@ def test_config_full(cfg, oracle):
         sums = out.sum(dim=1).cpu().numpy()
         assert np.all(np.abs(sums - mass) <= EPS / C), (cfg, b0, sums.min(), sums.max())
     pool.shutdown()
+
+
+@pytest.mark.parametrize("policy", ["uniform", "drop"])
+def test_ranked_layout_other_policies(policy):
+    """The ranked share layout of the B = 1 sweeps (share vectors > 64 MB) under
+    the Uniform and Drop policies: R-MAT 24 / ef 8, whole graph (ranked) against
+    the two-partition run (unranked CSRs) bit for bit, the policies' closed-form
+    masses (cpi_test.cpp:127-134; graph.cpp:265-268), and the ranked single-seed
+    query against the same seed's column of a batch (K3, unranked)."""
+    g = P.generate_rmat(24, 8, 0.57, 0.19, 0.19, rng_seed=5, policy=policy, device=0)
+    assert g.node_count() * 8 > (64 << 20)
+    art = P.preprocess(g, C, EPS, T)
+    st = art.stranger_scores
+    grp = P.PartitionGroup(g, [0, 0])
+    try:
+        assert np.array_equal(grp.preprocess(C, EPS, T), st), f"{policy}: partitioned preprocess differs"
+    finally:
+        grp.close()
+    pr = P.pagerank(g, P.CpiParams(C, EPS))
+    if policy == "uniform":
+        assert pr.iterations_run == 116 and pr.converged
+        assert abs(st.sum() - (1 - C) ** T) < EPS / C
+        assert abs(pr.scores.sum() - 1.0) < EPS / C
+    else:
+        assert pr.converged and pr.iterations_run <= 116
+        assert 0.0 < st.sum() < (1 - C) ** T  # mass leaks through the dangling nodes
+    seeds = P.sample_seeds(g, 32, 3)
+    qb = P.query_batch(g, art, seeds, S)
+    for k in (0, 17, 31):
+        assert_close(P.query(g, art, int(seeds[k]), S), qb[k], what=f"{policy} query {seeds[k]}")
