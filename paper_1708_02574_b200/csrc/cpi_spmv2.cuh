@@ -86,21 +86,6 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
 // kRanked: the ranked share layout (a.rank, tpa_gpu.cu): each share is stored
 // at its node's rank slot; gathers already read col_rank.
 
-// Deterministic CTA sum over kThr threads (fixed tree); valid in every thread.
-template <int kThr>
-__device__ __forceinline__ double mv_block_sum(double v, double* s_red) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    v = warp_sum(v);
-    __syncthreads();
-    if (lane == 0) s_red[w] = v;
-    __syncthreads();
-    double r = s_red[0];
-#pragma unroll
-    for (int k = 1; k < kThr / 32; ++k) r = dadd(r, s_red[k]);
-    __syncthreads();
-    return r;
-}
-
 constexpr int kMvFxSlots = 1;  // [4 x slots] fixed-point accumulators (w.fx, B = 1)
 // Consecutive sweeps are chained by programmatic dependent launch (C1 65.4 ->
 // 68.3 GTEPS: launch-bound sweeps); only thread 0 of a finished CTA takes the
@@ -115,7 +100,7 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     double* s_vals = reinterpret_cast<double*>(s_mv);
     int* s_rp = reinterpret_cast<int*>(s_vals + kNnz);  // row starts - nb
     double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + mv_rp_bytes<kRows>());
-    __shared__ double s_red[kThr / 32];
+    __shared__ double s_red[kThr / 32], s_l1[kThr / 32], s_dm[kThr / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t item = blockIdx.x;
@@ -191,8 +176,14 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         for (uint32_t r = tid; r < nrows; r += kThr) {
             const int lo = s_rp[r], hi = s_rp[r + 1];
             if (hi - lo <= kMvShortRow) {
+                // four loads ahead of their (still strictly sequential) adds
                 double s = 0.0;
-                for (int k = lo; k < hi; ++k) s = dadd(s, s_vals[k]);
+                int k = lo;
+                for (; k + 4 <= hi; k += 4) {
+                    const double a0 = s_vals[k], a1 = s_vals[k + 1], a2 = s_vals[k + 2], a3 = s_vals[k + 3];
+                    s = dadd(dadd(dadd(dadd(s, a0), a1), a2), a3);
+                }
+                for (; k < hi; ++k) s = dadd(s, s_vals[k]);
                 s_y[r] = s;
             }
         }
@@ -212,7 +203,9 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
                 if (lane == 0) s_y[rr] = s;
             }
         }
-        __syncthreads();
+        // a thread's rows r = tid + q * kThr were summed by itself (short rows)
+        // or by its own warp (r / 32 % (kThr / 32) == warp): no CTA barrier
+        __syncwarp();
         // epilogue with the prefetched degree / accumulator of each row
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
@@ -253,10 +246,14 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
             for (int j = 0; j < U; ++j) s = dadd(s, v[j]);
         }
         for (; e < ne; e += kThr) s = dadd(s, __ldg(a.share_in + ld_col(a.col + e)));
-        s = mv_block_sum<kThr>(s, s_red);
+        s = warp_sum(s);
+        if (lane == 0) s_red[warp] = s;
+        __syncthreads();
         if (tid == 0) {
             const uint32_t d = __ldg(a.deg + rb);
-            double y = s;
+            double y = s_red[0];  // the fixed tree: warp butterflies, then the warps in order
+#pragma unroll
+            for (int k = 1; k < kThr / 32; ++k) y = dadd(y, s_red[k]);
             if (st.has_spread) y = dadd(y, st.spread);  // graph.cpp:265-268
             if (a.y_out) a.y_out[rb] = y;
             if (a.acc) {
@@ -273,10 +270,24 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         }
     }
     {
-        // tile partials (fixed tree) -> exact fixed-point totals across tiles
-        const double tl1 = mv_block_sum<kThr>(my_l1, s_red);
-        const double tdm = want_dm ? mv_block_sum<kThr>(my_dm, s_red) : 0.0;
+        // tile partials (fixed tree: warp butterflies, then the warps in order)
+        // -> exact fixed-point totals across tiles; one barrier, thread 0 adds
+        // (a long row's partials are thread 0's alone: the tree adds zeros)
+        my_l1 = warp_sum(my_l1);
+        if (want_dm) my_dm = warp_sum(my_dm);
+        if (lane == 0) {
+            s_l1[warp] = my_l1;
+            s_dm[warp] = my_dm;
+        }
+        __syncthreads();
         if (tid == 0) {
+            double tl1 = s_l1[0], tdm = s_dm[0];
+#pragma unroll
+            for (int k = 1; k < kThr / 32; ++k) {
+                tl1 = dadd(tl1, s_l1[k]);
+                tdm = dadd(tdm, s_dm[k]);
+            }
+            if (!want_dm) tdm = 0.0;
             unsigned long long h = 0, l = 0;
             if (tl1 != 0.0) {
                 fx_add(h, l, tl1);
