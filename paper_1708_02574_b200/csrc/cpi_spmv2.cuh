@@ -66,6 +66,7 @@ struct MvArgs {
     unsigned long long* limbs;               // partition mode: [6] out (see fx_to_limbs), else null
     PeerOut peers;                           // partition group: replicas of share_out (n = 0: none)
     uint32_t limb_off;                       // limbs - share_out, in doubles (peer copies of the limbs)
+    uint32_t per_cta;                        // items per CTA, gridDim.x apart
 };
 
 // ColState after sweep `step` from the global residual / dangling mass
@@ -86,12 +87,24 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
 // kRanked: the ranked share layout (a.rank, tpa_gpu.cu): each share is stored
 // at its node's rank slot; gathers already read col_rank.
 
+// Items per CTA (gridDim.x apart): up to kMvItemsPerCta while the grid keeps
+// >= 256 CTAs per SM.  Measured per C4 PageRank sweep (ms; 408 k items, one
+// ticket + one set of total atomics per CTA instead of per tile):
+//   1: 2.853   3: 2.577   4: 2.538   6: 2.504   8: 2.494   10: 2.489
+// (C2, 16 k items: one item per CTA stays best, 0.097 ms.)
+constexpr uint32_t kMvItemsPerCta = 8;
+inline uint32_t mv_items_per_cta(uint32_t n_items, int num_sms) {
+    const uint32_t t = n_items / (uint32_t)(num_sms * 256);
+    return t < 1u ? 1u : (t > kMvItemsPerCta ? kMvItemsPerCta : t);
+}
 constexpr int kMvFxSlots = 1;  // [4 x slots] fixed-point accumulators (w.fx, B = 1)
 // Consecutive sweeps are chained by programmatic dependent launch (C1 65.4 ->
 // 68.3 GTEPS: launch-bound sweeps); only thread 0 of a finished CTA takes the
 // ticket (0.1102 -> 0.1097 ms per C2 sweep).  The default register
-// allocation (40, no minimum-blocks bound) measured best.
-template <bool kRanked, int kThr, int kNnz, int kRows>
+// allocation (no minimum-blocks bound) measured best in both forms.
+// kMulti: the CTA takes M.per_cta items (48 registers); otherwise exactly one
+// (40 registers, 12 CTAs per SM: the better form when the grid is small).
+template <bool kRanked, int kThr, int kNnz, int kRows, bool kMulti>
 __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     const StepArgs& a = M.s;
     // the tile's staging in dynamic shared memory (kMvDynSmem bytes): values,
@@ -101,34 +114,44 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     int* s_rp = reinterpret_cast<int*>(s_vals + kNnz);  // row starts - nb
     double* s_y = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_rp) + mv_rp_bytes<kRows>());
     __shared__ double s_red[kThr / 32], s_l1[kThr / 32], s_dm[kThr / 32];
+    __shared__ unsigned long long s_fx[4];  // the CTA's exact totals (thread 0 only)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t item = blockIdx.x;
-    // tile totals spread over kMvFxSlots accumulator pairs: fewer same-address
-    // atomics serialising in one L2 slice (the last CTA adds the slots)
-    const int fx_slot = (int)(item % kMvFxSlots);
+    // a CTA takes M.per_cta items, gridDim.x apart (the longest rows, first in
+    // the item list, stay spread over the grid): one ticket and one set of
+    // total atomics per CTA instead of per tile
     // programmatic dependent launch: the next sweep's CTAs may start once
     // every CTA of this one has; they wait below for this grid to finish
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const uint2 it = a.items[item];  // the tiling is static: read before the wait
-    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
-    const bool is_long = (it.y & kLongFlag) != 0;
-    const longlong2 nr = M.item_nnz[item];
-    const int64_t nb = nr.x, ne = nr.y;
+    uint2 it = a.items[blockIdx.x];  // the tiling is static: read before the wait
+    longlong2 nr = M.item_nnz[blockIdx.x];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous sweep's shares, acc, state
     const ColState st = a.state_in[0];
-    
+
     if (!st.active) {
         // column stopped earlier: only a pending combine remains (tpa.cpp:73)
         if (a.out)
-            for (uint32_t v = rb + tid; v < re; v += kThr) combine_only(a, v, 0, 1, v);
-        if (item == 0 && tid == 0) {
+            for (uint32_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+                const uint2 ii = a.items[item];
+                for (uint32_t v = ii.x + tid; v < (ii.y & ~kLongFlag); v += kThr) combine_only(a, v, 0, 1, v);
+            }
+        if (blockIdx.x == 0 && tid == 0) {
             a.state_out[0] = st;
             if (M.limbs)
                 for (int k = 0; k < 6; ++k) M.limbs[k] = 0ull;
         }
         return;
     }
+    if (kMulti && tid == 0) s_fx[0] = s_fx[1] = s_fx[2] = s_fx[3] = 0ull;
+  uint32_t item = blockIdx.x, t = 0;
+  do {
+    if (kMulti && t) {
+        it = a.items[item];
+        nr = M.item_nnz[item];
+    }
+    const uint32_t rb = it.x, re = it.y & ~kLongFlag;
+    const bool is_long = (it.y & kLongFlag) != 0;
+    const int64_t nb = nr.x, ne = nr.y;
     const bool want_dm = a.policy == kUniform;
     double my_l1 = 0.0, my_dm = 0.0;
     auto add_row = [&](double y, bool dangling) {
@@ -287,35 +310,40 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
                 tl1 = dadd(tl1, s_l1[k]);
                 tdm = dadd(tdm, s_dm[k]);
             }
-            if (!want_dm) tdm = 0.0;
-            unsigned long long h = 0, l = 0;
-            if (tl1 != 0.0) {
-                fx_add(h, l, tl1);
-                fx_atomic_add(&M.fx[4 * fx_slot + 0], &M.fx[4 * fx_slot + 1], h, l);
-            }
-            if (tdm != 0.0) {
-                h = l = 0;
-                fx_add(h, l, tdm);
-                fx_atomic_add(&M.fx[4 * fx_slot + 2], &M.fx[4 * fx_slot + 3], h, l);
+            if constexpr (kMulti) {
+                if (tl1 != 0.0) fx_add(s_fx[0], s_fx[1], tl1);
+                if (want_dm && tdm != 0.0) fx_add(s_fx[2], s_fx[3], tdm);
+            } else {
+                unsigned long long h = 0, l = 0;
+                if (tl1 != 0.0) {
+                    fx_add(h, l, tl1);
+                    fx_atomic_add(&M.fx[0], &M.fx[1], h, l);
+                }
+                if (want_dm && tdm != 0.0) {
+                    h = l = 0;
+                    fx_add(h, l, tdm);
+                    fx_atomic_add(&M.fx[2], &M.fx[3], h, l);
+                }
             }
         }
     }
+    if constexpr (!kMulti) break;
+    ++t;
+    item += gridDim.x;
+  } while (t < M.per_cta && item < a.n_items);  // the CTA's items
     // only thread 0 takes the ticket: the rest of the CTA leaves now instead
     // of waiting out the fence + atomic round trip
     if (tid != 0) return;
+    if constexpr (kMulti) {
+        if (s_fx[0] | s_fx[1]) fx_atomic_add(&M.fx[0], &M.fx[1], s_fx[0], s_fx[1]);
+        if (s_fx[2] | s_fx[3]) fx_atomic_add(&M.fx[2], &M.fx[3], s_fx[2], s_fx[3]);
+    }
     __threadfence();
     if (atomicAdd(a.done_cnt, 1u) != gridDim.x - 1) return;
     __threadfence();
-    // exact 128-bit sums of the slots (order-free)
-    unsigned long long h0 = 0, l0 = 0, h1 = 0, l1 = 0;
-    for (int k = 0; k < kMvFxSlots; ++k) {
-        const unsigned long long a0 = atomicAdd(&M.fx[4 * k + 0], 0ull), b0 = atomicAdd(&M.fx[4 * k + 1], 0ull);
-        const unsigned long long a1 = atomicAdd(&M.fx[4 * k + 2], 0ull), b1 = atomicAdd(&M.fx[4 * k + 3], 0ull);
-        l0 += b0;
-        h0 += a0 + (l0 < b0 ? 1ull : 0ull);
-        l1 += b1;
-        h1 += a1 + (l1 < b1 ? 1ull : 0ull);
-    }
+    // exact 128-bit sums (order-free)
+    const unsigned long long h0 = atomicAdd(&M.fx[0], 0ull), l0 = atomicAdd(&M.fx[1], 0ull);
+    const unsigned long long h1 = atomicAdd(&M.fx[2], 0ull), l1 = atomicAdd(&M.fx[3], 0ull);
     if (M.limbs) {
         // a partition's totals: all-reduced, then k_part_finalize advances the state
         fx_to_limbs(h0, l0, M.limbs);

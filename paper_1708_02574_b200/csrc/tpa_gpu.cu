@@ -746,11 +746,18 @@ static size_t seg_of(const std::vector<uint32_t>& bounds, uint32_t i) {
 
 // K2 v2 at one tile shape: dynamic shared memory sized for it, set once per
 // instantiation.
+template <bool RF, int THR, int NNZ, int ROWS, bool MULTI>
+static void launch_mv2_(const MvArgs& M, uint32_t grid, cudaStream_t stream);
 template <bool RF, int THR, int NNZ, int ROWS>
 static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
+    if (M.per_cta > 1) launch_mv2_<RF, THR, NNZ, ROWS, true>(M, grid, stream);
+    else launch_mv2_<RF, THR, NNZ, ROWS, false>(M, grid, stream);
+}
+template <bool RF, int THR, int NNZ, int ROWS, bool MULTI>
+static void launch_mv2_(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
     constexpr size_t smem = mv_dyn_smem<NNZ, ROWS>();
     static const bool ok = [] {
-        CK(cudaFuncSetAttribute(k_step_spmv2<RF, THR, NNZ, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_step_spmv2<RF, THR, NNZ, ROWS, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
         return true;
     }();
@@ -765,7 +772,7 @@ static void launch_mv2(const MvArgs& M, uint32_t grid, cudaStream_t stream) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, k_step_spmv2<RF, THR, NNZ, ROWS>, M));  // programmatic dependent launch
+    CK(cudaLaunchKernelEx(&cfg, k_step_spmv2<RF, THR, NNZ, ROWS, MULTI>, M));  // programmatic dependent launch
 }
 
 static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmArgs* mm, int B,
@@ -873,16 +880,17 @@ static void launch_step(tpa_graph* g, Workspace& w, const StepArgs& a, const MmA
                          !g->part ? nullptr
                          : a.share_out ? reinterpret_cast<unsigned long long*>(a.share_out + g->part->slice)
                                        : w.limbs.as<unsigned long long>() + (a.step & 1) * 6,
-                         PeerOut{}, g->part ? g->part->slice : 0u};
+                         PeerOut{}, g->part ? g->part->slice : 0u, mv_items_per_cta(s.n_items, g->num_sms)};
                 if (g->part && a.share_out) M.peers = g->peer_out;
+                const uint32_t mv_grid = (s.n_items + M.per_cta - 1) / M.per_cta;
                 const MvShape& sh = g->mv_shape;
                 const bool ranked = a.rank != nullptr;
                 if (sh.thr == kMvShapeS.thr && sh.nnz == kMvShapeS.nnz && sh.rows == kMvShapeS.rows) {
-                    if (ranked) launch_mv2<true, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
-                    else launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, grid.x, g->stream);
+                    if (ranked) launch_mv2<true, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, mv_grid, g->stream);
+                    else launch_mv2<false, kMvShapeS.thr, kMvShapeS.nnz, kMvShapeS.rows>(M, mv_grid, g->stream);
                 } else {
-                    if (ranked) launch_mv2<true, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
-                    else launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, grid.x, g->stream);
+                    if (ranked) launch_mv2<true, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, mv_grid, g->stream);
+                    else launch_mv2<false, kMvShapeL.thr, kMvShapeL.nnz, kMvShapeL.rows>(M, mv_grid, g->stream);
                 }
             }
             break;
