@@ -144,8 +144,24 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     }
     if (kMulti && tid == 0) s_fx[0] = s_fx[1] = s_fx[2] = s_fx[3] = 0ull;
   uint32_t item = blockIdx.x, t = 0;
+  // kMulti: a tile's column indices are requested before the barrier that ends
+  // the previous tile, so that round trip overlaps the wait for its slowest warp
+  // (the 128-thread shape only: C4 2.488 -> 2.449 ms; the 256-thread shape of C5
+  // loses a resident CTA to the longer-lived registers, 33.5 -> 35.1 ms)
+  constexpr bool kAhead = kMulti && kThr == 128;
+  uint32_t u[kNnz / kThr];
+  auto prefetch_idx = [&](const uint2& ii, const longlong2& rr) {
+      if (ii.y & kLongFlag) return;  // a long row streams its own indices
+      const int nnz = (int)(rr.y - rr.x);
+#pragma unroll
+      for (int j = 0; j < kNnz / kThr; ++j) {
+          const int k = tid + j * kThr;
+          u[j] = k < nnz ? ld_col(a.col + rr.x + k) : 0u;
+      }
+  };
+  if constexpr (kAhead) prefetch_idx(it, nr);
   do {
-    if (kMulti && t) {
+    if (kMulti && !kAhead && t) {
         it = a.items[item];
         nr = M.item_nnz[item];
     }
@@ -165,12 +181,7 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         constexpr int U = kNnz / kThr;
         constexpr int RPT = kRows / kThr;  // rows per thread
         // ---- round trip 1: indices, row pointers, degrees, accumulators ----
-        uint32_t u[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const int k = tid + j * kThr;
-            u[j] = k < nnz ? ld_col(a.col + nb + k) : 0u;
-        }
+        if constexpr (!kAhead) prefetch_idx(it, nr);
         for (uint32_t r = tid; r <= nrows; r += kThr) s_rp[r] = (int)(__ldg(a.row_ptr + rb + r) - nb);
         uint32_t dg[RPT], so[RPT];
         double ac[RPT];
@@ -301,6 +312,13 @@ __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
         if (lane == 0) {
             s_l1[warp] = my_l1;
             s_dm[warp] = my_dm;
+        }
+        if constexpr (kAhead) {
+            if (t + 1 < M.per_cta && item + gridDim.x < a.n_items) {
+                it = a.items[item + gridDim.x];
+                nr = M.item_nnz[item + gridDim.x];
+                prefetch_idx(it, nr);
+            }
         }
         __syncthreads();
         if (tid == 0) {
