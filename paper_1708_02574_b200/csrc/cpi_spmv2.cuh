@@ -13,7 +13,10 @@
 //     partitioned run reproduces the one-GPU residuals bit for bit.  The last
 //     CTA advances the state, or, for a partition, publishes its totals as
 //     carry-free limbs for an all-reduce (fx_to_limbs) and leaves the state
-//     to k_part_finalize.
+//     to k_part_finalize;
+//   * on large grids a CTA takes several tiles (kMulti): the per-tile partials
+//     meet in the CTA's exact totals in shared memory, and the total atomics,
+//     the fence and the ticket are paid once per CTA.
 #pragma once
 
 #include "cpi_spmm.cuh"
@@ -102,8 +105,9 @@ constexpr int kMvFxSlots = 1;  // [4 x slots] fixed-point accumulators (w.fx, B 
 // 68.3 GTEPS: launch-bound sweeps); only thread 0 of a finished CTA takes the
 // ticket (0.1102 -> 0.1097 ms per C2 sweep).  The default register
 // allocation (no minimum-blocks bound) measured best in both forms.
-// kMulti: the CTA takes M.per_cta items (48 registers); otherwise exactly one
-// (40 registers, 12 CTAs per SM: the better form when the grid is small).
+// kMulti: the CTA takes M.per_cta items (48 registers, 56 with the index
+// look-ahead of the 128-thread shape); otherwise exactly one (40 registers,
+// 12 CTAs per SM: the better form when the grid is small).
 template <bool kRanked, int kThr, int kNnz, int kRows, bool kMulti>
 __global__ void __launch_bounds__(kThr) k_step_spmv2(MvArgs M) {
     const StepArgs& a = M.s;
