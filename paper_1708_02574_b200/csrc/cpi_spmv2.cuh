@@ -91,13 +91,14 @@ __device__ __forceinline__ ColState advance_state(ColState s, double res, double
 // at its node's rank slot; gathers already read col_rank.
 
 // Items per CTA (gridDim.x apart): up to kMvItemsPerCta while the grid keeps
-// >= 256 CTAs per SM.  Measured per C4 PageRank sweep (ms; 408 k items, one
+// >= 64 CTAs per SM.  Measured per C4 PageRank sweep (ms; 408 k items, one
 // ticket + one set of total atomics per CTA instead of per tile):
 //   1: 2.853   3: 2.577   4: 2.538   6: 2.504   8: 2.494   10: 2.489
-// (C2, 16 k items: one item per CTA stays best, 0.097 ms.)
+// C3 (65 k items): 1: 0.403   3: 0.362   6: 0.351   8: 0.353;  C2 (16 k items):
+// one item per CTA stays best (0.096 ms; 3: 0.099).
 constexpr uint32_t kMvItemsPerCta = 8;
 inline uint32_t mv_items_per_cta(uint32_t n_items, int num_sms) {
-    const uint32_t t = n_items / (uint32_t)(num_sms * 256);
+    const uint32_t t = n_items / (uint32_t)(num_sms * 64);
     return t < 1u ? 1u : (t > kMvItemsPerCta ? kMvItemsPerCta : t);
 }
 constexpr int kMvFxSlots = 1;  // [4 x slots] fixed-point accumulators (w.fx, B = 1)
